@@ -1,0 +1,143 @@
+/*
+ * btd.h -- C ABI of the B200 (sm_100a) nested-dissection block-tridiagonal Cholesky library.
+ *
+ * Problem (§3): Psi is symmetric positive definite block
+ * tridiagonal with N diagonal blocks D_i (n x n, symmetric) and N-1 coupling
+ * blocks E_i at block position (i+1, i). The library computes the multi-stage
+ * (nested-dissection) factorization P Psi P^T = L^ L^^T (PAPER.md:486-560,
+ * Algorithm 4; permutation P_inf of PAPER.md:488-508) and solves Psi x = b
+ * with the level sweeps of Algorithm 6, for one system or a
+ * batch of independent systems. Every step runs in hand-written CUDA kernels.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions shared by all calls
+ * ---------------------------------------------------------------------------
+ * Indices. Original block indices are 1-based, i = 1..N. Level l = 1..L with
+ * L = floor(log2 N) + 1 and stride s = 2^(l-1); the columns
+ * eliminated at level l are i = s, 3s, 5s, ... <= N.
+ *
+ * Layouts (all arrays contiguous, batch outermost, blocks row-major):
+ *   D    [batch][N][n][n]     only the lower triangle of each block is read
+ *   E    [batch][N-1][n][n]   E[k-1] is block (k+1, k) of Psi
+ *   Dhat [batch][N][n][n]     Dhat[i-1] = diagonal block of L^ for original block i;
+ *                             lower triangular, strict upper written as exact zeros
+ *   C    [batch][nC][n][n]    coupling blocks, nC = btd_num_coupling_blocks()
+ *   b, x [batch][N][n][m]
+ * Coupling slot (l, k), k = 1 .. floor(N/s) - 1, lives at index
+ * off(l) + k - 1 with off(l) = sum_{l' < l} (floor(N / 2^(l'-1)) - 1)
+ * (level-major, k ascending). It couples original blocks a = k s and
+ * b = (k+1) s and holds block (b, a) of M + M^T, where M is L^ with rows and
+ * columns relabelled by original block index ("Psi-lower orientation",
+ * SURVEY.md §8(c) A2). For odd k the column a is eliminated at level l and the
+ * slot holds the L^ block (b, a) = E^_{l,k} D^_a^{-T}-form of Alg. 4 l.10; for
+ * even k the column b is eliminated at level l and the slot holds the
+ * transpose of L^ block (a, b), i.e. D^_b^{-1} E^_{l,k} of Alg. 4 l.12. Slots
+ * of level l >= 2 are the fill blocks of Alg. 4 l.13 (the paper's E^ first
+ * subscript is read as the level). Level 1 slots
+ * correspond one to one to E.
+ *
+ * Precision. BTD_F32 computes in binary32, BTD_F64 in binary64, end to end
+ * (FMA contraction allowed, no TF32). Block sizes n that
+ * are not a compiled size are padded internally with an identity diagonal,
+ * which changes no output value.
+ *
+ * Memory and streams. The caller allocates every buffer (device memory unless
+ * a name says host). The library never allocates device memory. Every call
+ * taking a stream is asynchronous on that stream (a cudaStream_t passed as
+ * void*, NULL = legacy default stream) and never synchronises it. In-place use
+ * is allowed: Dhat may alias D, and the first N-1 blocks of C may alias E.
+ *
+ * Errors. Return values report argument and launch errors only. Numerical
+ * failure is reported per system in device memory, LAPACK style: info[j] = 0
+ * on success, otherwise the 1-based original index of the failing pivot block
+ * (pivot <= 0 or NaN); if several blocks fail
+ * the one with the smallest (level, index) is reported. Outputs of a failed
+ * system are unspecified.
+ */
+#ifndef BTD_H
+#define BTD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct btd_plan btd_plan; /* host-only, immutable after create, thread-safe to share */
+
+typedef enum { BTD_F32 = 0, BTD_F64 = 1 } btd_dtype;
+
+typedef enum {
+    BTD_OK = 0,
+    BTD_EINVAL = 1,      /* bad argument (null pointer, size out of range, misaligned buffer) */
+    BTD_ECUDA = 2,       /* a CUDA runtime call or kernel launch failed */
+    BTD_ENOMEM = 3,      /* host allocation for the plan failed */
+    BTD_EUNSUPPORTED = 4 /* size outside what this build supports (n > 128) */
+} btd_status;
+
+/* Variant selector (btd_plan_create_ex). AUTO picks by size. */
+typedef enum {
+    BTD_VARIANT_AUTO = 0,
+    BTD_VARIANT_FUSED = 1, /* one CTA per system, all levels + both sweeps in one launch, state in smem */
+    BTD_VARIANT_LEVEL = 2  /* one launch per level (Alg. 4 deferred form), state in the output buffers */
+} btd_variant;
+
+/* Create a plan for `batch` systems of N blocks of size n with m right-hand sides.
+ * Requires N >= 1, 1 <= n <= 128, batch >= 1, m >= 1. The plan is the symbolic
+ * analysis of a0: levels, slot offsets and kernel choice,
+ * all derived from (N, n, batch, m, dtype) alone. */
+btd_status btd_plan_create(btd_plan **out, int64_t N, int64_t n, int64_t batch, int64_t m,
+                           btd_dtype dtype);
+btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batch, int64_t m,
+                              btd_dtype dtype, btd_variant variant);
+void btd_plan_destroy(btd_plan *plan);
+
+/* floor(log2 N) + 1. */
+int32_t btd_num_levels(const btd_plan *plan);
+/* Coupling blocks per system: sum_l (floor(N/2^(l-1)) - 1) = (N-1) + (#interior eliminations). */
+int64_t btd_num_coupling_blocks(const btd_plan *plan);
+/* Offset of level l's first slot (1 <= l <= L+1; l = L+1 returns the total). -1 if out of range. */
+int64_t btd_level_offset(const btd_plan *plan, int32_t level);
+/* P_inf as host array perm[new position] = original index, both 0-based. */
+btd_status btd_permutation(const btd_plan *plan, int64_t *host_perm);
+/* The variant the plan will launch (BTD_VARIANT_FUSED or BTD_VARIANT_LEVEL). */
+int32_t btd_plan_variant(const btd_plan *plan);
+/* Number of kernel launches one call of factor / solve / factor_solve makes (op = 0 / 1 / 2). */
+int32_t btd_plan_launches(const btd_plan *plan, int32_t op);
+/* Bytes of dynamic shared memory per CTA of the fused kernel (0 for the level variant). */
+int64_t btd_plan_smem_bytes(const btd_plan *plan);
+
+/* Factorization P Psi P^T = L^ L^^T (Algorithm 4). Device pointers D, E (E may be
+ * NULL when N = 1), Dhat, C, info[batch]. */
+btd_status btd_factor(const btd_plan *plan, const void *D, const void *E, void *Dhat, void *C,
+                      int32_t *info, void *stream);
+
+/* Solve Psi x = b with a factor from btd_factor (Algorithm 6). b may alias x. */
+btd_status btd_solve(const btd_plan *plan, const void *Dhat, const void *C, const void *b, void *x,
+                     void *stream);
+
+/* Factor and solve in one call; the forward sweep is interlaced with the factorization
+ * (PAPER.md:672-676, 755). Writes Dhat, C, x and info. */
+btd_status btd_factor_solve(const btd_plan *plan, const void *D, const void *E, const void *b,
+                            void *Dhat, void *C, void *x, int32_t *info, void *stream);
+
+/* End-to-end variant with HOST inputs and outputs: copies host_D/host_E/host_b
+ * (page-locked recommended) to the caller's device buffers dev_D/dev_E/dev_b,
+ * runs btd_factor_solve, and copies Dhat, C, x and info back to the host
+ * arrays, all on `stream`. The batch is processed in `chunks` slices so that
+ * copies of one slice overlap compute of another (chunks >= 1; the device
+ * buffers must hold the whole batch). Asynchronous like every other call. */
+btd_status btd_factor_solve_host(const btd_plan *plan, const void *host_D, const void *host_E,
+                                 const void *host_b, void *host_Dhat, void *host_C, void *host_x,
+                                 int32_t *host_info, void *dev_D, void *dev_E, void *dev_b,
+                                 void *dev_Dhat, void *dev_C, void *dev_x, int32_t *dev_info,
+                                 int32_t chunks, void *stream);
+
+const char *btd_status_string(btd_status status);
+/* Last CUDA error string observed by this thread inside the library (or ""). */
+const char *btd_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BTD_H */

@@ -1,0 +1,78 @@
+"""Build libbtd.so (the C-ABI library of include/btd.h) for sm_100a, in-tree.
+
+The typed kernels are split into one translation unit per (dtype, compiled block size) so
+the 20 instantiations compile in parallel. Usage: ``python -m paper_2601_03754_b200.build``.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
+LIB = os.path.join(HERE, "libbtd.so")
+ROOT = os.path.dirname(HERE)
+
+SIZES = [1, 2, 3, 4, 6, 8, 12, 16, 24, 32]
+DTYPES = ["float", "double"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
+         "-I" + os.path.join(ROOT, "include")]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
+            return cand
+    return "nvcc"
+
+
+def _sources() -> list[str]:
+    out = [os.path.join(ROOT, "include", "btd.h")]
+    for f in os.listdir(CSRC):
+        out.append(os.path.join(CSRC, f))
+    return out
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(args: tuple[str, list[str], str]) -> str:
+    src, defs, obj = args
+    cmd = [_nvcc(), *ARCH, *FLAGS, *defs, "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {obj}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return (r.stderr or "").strip()
+
+
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+    deps = _sources()
+    if not force and not _stale(LIB, deps):
+        return LIB
+    os.makedirs(OBJ, exist_ok=True)
+    units = [(os.path.join(CSRC, "btd.cu"), [], os.path.join(OBJ, "btd.o"))]
+    for dt in DTYPES:
+        for nb in SIZES:
+            units.append((os.path.join(CSRC, "btd_inst.cu"), [f"-DBTD_T={dt}", f"-DBTD_NB={nb}"],
+                          os.path.join(OBJ, f"btd_inst_{dt}_{nb}.o")))
+    todo = [u for u in units if force or _stale(u[2], deps)]
+    jobs = jobs or max(1, os.cpu_count() or 1)
+    with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
+        for (src, defs, obj), msg in zip(todo, ex.map(_compile, todo)):
+            if verbose and msg:
+                print(f"[{os.path.basename(obj)}] {msg}", file=sys.stderr)
+    cmd = [_nvcc(), *ARCH, "-shared", "-o", LIB, *[u[2] for u in units]]
+    subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

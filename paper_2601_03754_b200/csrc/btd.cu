@@ -1,0 +1,209 @@
+// btd.cu -- C ABI (include/btd.h): plan (symbolic analysis a0), argument checks, dispatch.
+//
+// The plan derives everything from (N, n, batch, m, dtype): L = floor(log2 N)+1 levels
+// (PAPER.md:569), slot offsets off(l) = sum_{l'<l} (floor(N/2^(l'-1)) - 1), the compiled block
+// size NB >= n (identity padding), the team width and the kernel variant. No device tables:
+// every index is closed form in (level, column) and passed as kernel arguments.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "btd_internal.h"
+
+using namespace btd;
+
+static thread_local char g_last_error[256] = "";
+
+btd_status btd::record_cuda_error(cudaError_t e) {
+    snprintf(g_last_error, sizeof g_last_error, "%s", cudaGetErrorString(e));
+    return BTD_ECUDA;
+}
+static btd_status cuda_fail(cudaError_t e) { return record_cuda_error(e); }
+
+static const int kSizes[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+
+static int pick_nb(int64_t n) {
+    for (int s : kSizes)
+        if (n <= s) return s;
+    return -1;
+}
+
+template <typename T>
+static btd_status run_dtype(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat,
+                            void *C, void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    switch (p->NB) {
+#define BTD_CASE(S) \
+    case S: return run_typed<T, S>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+        BTD_CASE(1) BTD_CASE(2) BTD_CASE(3) BTD_CASE(4) BTD_CASE(6) BTD_CASE(8) BTD_CASE(12) BTD_CASE(16)
+        BTD_CASE(24) BTD_CASE(32)
+#undef BTD_CASE
+        default: return BTD_EUNSUPPORTED;
+    }
+}
+
+template <typename T>
+static size_t fused_bytes_dt(const btd_plan *p, bool fact, bool solve) {
+    switch (p->NB) {
+#define BTD_CASE(S) \
+    case S: return fused_bytes<T, S>(p, fact, solve);
+        BTD_CASE(1) BTD_CASE(2) BTD_CASE(3) BTD_CASE(4) BTD_CASE(6) BTD_CASE(8) BTD_CASE(12) BTD_CASE(16)
+        BTD_CASE(24) BTD_CASE(32)
+#undef BTD_CASE
+        default: return ~(size_t)0;
+    }
+}
+
+static btd_status run(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
+                      void *x, int32_t *info, int64_t sys0, int64_t count, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->dtype == BTD_F32) return run_dtype<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    return run_dtype<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batch, int64_t m, btd_dtype dtype,
+                              btd_variant variant) {
+    if (!out) return BTD_EINVAL;
+    *out = nullptr;
+    if (N < 1 || n < 1 || batch < 1 || m < 1 || (dtype != BTD_F32 && dtype != BTD_F64)) return BTD_EINVAL;
+    if (N > (1ll << 24) || m > 4096) return BTD_EINVAL;
+    const int NB = pick_nb(n);
+    if (NB < 0) return BTD_EUNSUPPORTED;
+    btd_plan *p = new (std::nothrow) btd_plan();
+    if (!p) return BTD_ENOMEM;
+    p->N = N; p->n = n; p->batch = batch; p->m = m; p->dtype = dtype; p->NB = NB;
+    int L = 0;
+    while ((1ll << L) <= N) ++L;  // floor(log2 N) + 1
+    p->L = L;
+    memset(&p->geo, 0, sizeof p->geo);
+    p->geo.N = (int)N; p->geo.n = (int)n; p->geo.m = (int)m; p->geo.L = L;
+    long long off = 0;
+    for (int l = 1; l <= L + 1; ++l) {
+        p->geo.off[l - 1] = off;
+        if (l <= L) off += (N >> (l - 1)) - 1;
+    }
+    p->geo.nC = off;
+    const bool f32 = dtype == BTD_F32;
+    p->smem_fs = f32 ? fused_bytes_dt<float>(p, true, true) : fused_bytes_dt<double>(p, true, true);
+    p->smem_f = f32 ? fused_bytes_dt<float>(p, true, false) : fused_bytes_dt<double>(p, true, false);
+    p->smem_s = f32 ? fused_bytes_dt<float>(p, false, true) : fused_bytes_dt<double>(p, false, true);
+    const bool fits = p->smem_fs <= kMaxSmem;
+    if (variant == BTD_VARIANT_FUSED && !fits) {
+        delete p;
+        return BTD_EUNSUPPORTED;
+    }
+    p->variant = (variant == BTD_VARIANT_LEVEL || (variant == BTD_VARIANT_AUTO && !fits)) ? BTD_VARIANT_LEVEL
+                                                                                           : BTD_VARIANT_FUSED;
+    *out = p;
+    return BTD_OK;
+}
+
+btd_status btd_plan_create(btd_plan **out, int64_t N, int64_t n, int64_t batch, int64_t m, btd_dtype dtype) {
+    return btd_plan_create_ex(out, N, n, batch, m, dtype, BTD_VARIANT_AUTO);
+}
+
+void btd_plan_destroy(btd_plan *plan) { delete plan; }
+
+int32_t btd_num_levels(const btd_plan *p) { return p ? p->L : -1; }
+
+int64_t btd_num_coupling_blocks(const btd_plan *p) { return p ? p->geo.nC : -1; }
+
+int64_t btd_level_offset(const btd_plan *p, int32_t level) {
+    if (!p || level < 1 || level > p->L + 1) return -1;
+    return p->geo.off[level - 1];
+}
+
+btd_status btd_permutation(const btd_plan *p, int64_t *host_perm) {
+    if (!p || !host_perm) return BTD_EINVAL;
+    int64_t q = 0;
+    for (int l = 1; l <= p->L; ++l) {
+        const int64_t s = 1ll << (l - 1);
+        for (int64_t c = s; c <= p->N; c += 2 * s) host_perm[q++] = c - 1;
+    }
+    return BTD_OK;
+}
+
+int32_t btd_plan_variant(const btd_plan *p) { return p ? p->variant : -1; }
+
+int32_t btd_plan_launches(const btd_plan *p, int32_t op) {
+    if (!p || op < 0 || op > 2) return -1;
+    if (p->variant == BTD_VARIANT_FUSED) return 1;
+    const int64_t chunks = (p->batch + 65534) / 65535;
+    const int per = op == 0 ? p->L : op == 1 ? 2 * p->L : 2 * p->L;
+    return (int32_t)(1 + chunks * per);
+}
+
+int64_t btd_plan_smem_bytes(const btd_plan *p) {
+    if (!p) return -1;
+    return p->variant == BTD_VARIANT_FUSED ? (int64_t)p->smem_fs : 0;
+}
+
+btd_status btd_factor(const btd_plan *p, const void *D, const void *E, void *Dhat, void *C, int32_t *info,
+                      void *stream) {
+    if (!p || !D || !Dhat || !C || !info || (p->N > 1 && !E)) return BTD_EINVAL;
+    return run(p, 0, D, E, nullptr, Dhat, C, nullptr, info, 0, p->batch, stream);
+}
+
+btd_status btd_solve(const btd_plan *p, const void *Dhat, const void *C, const void *b, void *x, void *stream) {
+    if (!p || !Dhat || !C || !b || !x) return BTD_EINVAL;
+    return run(p, 1, nullptr, nullptr, b, (void *)Dhat, (void *)C, x, nullptr, 0, p->batch, stream);
+}
+
+btd_status btd_factor_solve(const btd_plan *p, const void *D, const void *E, const void *b, void *Dhat, void *C,
+                            void *x, int32_t *info, void *stream) {
+    if (!p || !D || !b || !Dhat || !C || !x || !info || (p->N > 1 && !E)) return BTD_EINVAL;
+    return run(p, 2, D, E, b, Dhat, C, x, info, 0, p->batch, stream);
+}
+
+btd_status btd_factor_solve_host(const btd_plan *p, const void *hD, const void *hE, const void *hb, void *hDhat,
+                                 void *hC, void *hx, int32_t *hinfo, void *dD, void *dE, void *db, void *dDhat,
+                                 void *dC, void *dx, int32_t *dinfo, int32_t chunks, void *stream) {
+    if (!p || !hD || !hb || !hDhat || !hC || !hx || !hinfo || !dD || !db || !dDhat || !dC || !dx || !dinfo ||
+        chunks < 1)
+        return BTD_EINVAL;
+    if (p->N > 1 && (!hE || !dE)) return BTD_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t w = p->dtype == BTD_F32 ? 4 : 8;
+    const size_t nn = (size_t)p->n * p->n;
+    const size_t sD = p->N * nn * w, sE = (p->N - 1) * nn * w, sb = p->N * p->n * p->m * w,
+                 sC = (size_t)p->geo.nC * nn * w;
+    const int64_t per = (p->batch + chunks - 1) / chunks;
+    for (int64_t s0 = 0; s0 < p->batch; s0 += per) {
+        const int64_t cnt = (p->batch - s0) < per ? (p->batch - s0) : per;
+        cudaError_t e;
+#define CP(dst, src, bytes, kind)                                   \
+    e = cudaMemcpyAsync((dst), (src), (bytes), kind, st);           \
+    if (e != cudaSuccess) return cuda_fail(e);
+        CP((char *)dD + s0 * sD, (const char *)hD + s0 * sD, cnt * sD, cudaMemcpyHostToDevice);
+        if (sE) CP((char *)dE + s0 * sE, (const char *)hE + s0 * sE, cnt * sE, cudaMemcpyHostToDevice);
+        CP((char *)db + s0 * sb, (const char *)hb + s0 * sb, cnt * sb, cudaMemcpyHostToDevice);
+        btd_status rs = run(p, 2, dD, dE, db, dDhat, dC, dx, dinfo, s0, cnt, stream);
+        if (rs != BTD_OK) return rs;
+        CP((char *)hDhat + s0 * sD, (const char *)dDhat + s0 * sD, cnt * sD, cudaMemcpyDeviceToHost);
+        if (sC) CP((char *)hC + s0 * sC, (const char *)dC + s0 * sC, cnt * sC, cudaMemcpyDeviceToHost);
+        CP((char *)hx + s0 * sb, (const char *)dx + s0 * sb, cnt * sb, cudaMemcpyDeviceToHost);
+        CP(hinfo + s0, dinfo + s0, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost);
+#undef CP
+    }
+    return BTD_OK;
+}
+
+const char *btd_status_string(btd_status s) {
+    switch (s) {
+        case BTD_OK: return "BTD_OK";
+        case BTD_EINVAL: return "BTD_EINVAL: invalid argument";
+        case BTD_ECUDA: return "BTD_ECUDA: CUDA error";
+        case BTD_ENOMEM: return "BTD_ENOMEM: host allocation failed";
+        case BTD_EUNSUPPORTED: return "BTD_EUNSUPPORTED: size not supported by this build";
+    }
+    return "BTD_UNKNOWN";
+}
+
+const char *btd_last_error(void) { return g_last_error; }
+
+}  // extern "C"

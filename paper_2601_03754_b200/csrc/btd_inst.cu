@@ -1,0 +1,97 @@
+// btd_inst.cu -- typed launchers; compiled once per (dtype, NB) with -DBTD_T=<float|double> -DBTD_NB=<n>
+// so the 20 instantiations build in parallel (see paper_2601_03754_b200/build.py).
+#include "btd_internal.h"
+
+namespace btd {
+static btd_status cuda_fail(cudaError_t e) { return record_cuda_error(e); }
+
+template <typename T, int NB, bool FACT, bool SOLVE>
+static btd_status launch_fused(const btd_plan *p, const T *D, const T *E, const T *b, T *Dhat, T *C, T *x,
+                               int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    constexpr int TS = TeamShape<NB>::TS, NT = TeamShape<NB>::NT;
+    auto kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE>;
+    const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+        if (e != cudaSuccess) return cuda_fail(e);
+        attr_set = true;
+    }
+    for (int64_t s0 = 0; s0 < count; s0 += (1ll << 30)) {
+        const int64_t cnt = (count - s0) < (1ll << 30) ? (count - s0) : (1ll << 30);
+        kern<<<(unsigned)cnt, NT * TS, smem, st>>>(D, E, b, Dhat, C, x, info, p->geo, (int)(sys0 + s0));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    return BTD_OK;
+}
+
+template <typename T, int NB, bool FACT, bool SOLVE>
+static btd_status launch_level(const btd_plan *p, const T *D, const T *E, const T *b, T *Dhat, T *C, T *x,
+                               int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    constexpr int TS = LevelShape<T, NB>::TS, NT = LevelShape<T, NB>::NT;
+    constexpr int SMEM = NT * LevelShape<T, NB>::BYTES;
+    const int64_t N = p->N, n = p->n, m = p->m;
+    const size_t nn = (size_t)n * n;
+    {   // init: Dhat <- D, x <- b, info <- 0 (for the slice)
+        const long long nD = FACT ? (long long)(count * N * nn) : 0;
+        const long long nb = SOLVE ? (long long)(count * N * n * m) : 0;
+        long long work = nD > nb ? nD : nb;
+        if (work < count) work = count;
+        int blocks = (int)((work + 255) / 256);
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        if (blocks < 1) blocks = 1;
+        btd_level_init_kernel<T><<<blocks, 256, 0, st>>>(
+            FACT ? D + sys0 * N * nn : nullptr, SOLVE ? b + sys0 * N * n * m : nullptr,
+            FACT ? Dhat + sys0 * N * nn : nullptr, SOLVE ? x + sys0 * N * n * m : nullptr,
+            FACT ? info + sys0 : nullptr, nD, nb, (int)count, FACT ? 1 : 0, SOLVE ? 1 : 0);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    for (int64_t s0 = 0; s0 < count; s0 += 65535) {
+        const int64_t cnt = (count - s0) < 65535 ? (count - s0) : 65535;
+        const int base = (int)(sys0 + s0);
+        for (int l = 1; l <= p->L; ++l) {
+            const int64_t s = 1ll << (l - 1);
+            const int64_t ncols = ((N / s) + 1) / 2;
+            dim3 grid((unsigned)((ncols + NT - 1) / NT), (unsigned)cnt);
+            btd_level_fwd_kernel<T, NB, TS, NT, FACT, SOLVE>
+                <<<grid, NT * TS, SMEM, st>>>(E, Dhat, C, x, info, p->geo, l, base);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+        if (SOLVE) {
+            for (int l = p->L; l >= 1; --l) {
+                const int64_t s = 1ll << (l - 1);
+                const int64_t ncols = ((N / s) + 1) / 2;
+                dim3 grid((unsigned)((ncols + NT - 1) / NT), (unsigned)cnt);
+                btd_level_bwd_kernel<T, NB, TS, NT><<<grid, NT * TS, 0, st>>>(Dhat, C, x, p->geo, l, base);
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return cuda_fail(e);
+            }
+        }
+    }
+    return BTD_OK;
+}
+
+template <typename T, int NB>
+btd_status run_typed(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat,
+                            void *C, void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    const T *Dt = (const T *)D, *Et = (const T *)E, *bt = (const T *)b;
+    T *Dh = (T *)Dhat, *Ct = (T *)C, *xt = (T *)x;
+    if (p->variant == BTD_VARIANT_FUSED) {
+        if (op == 0) return launch_fused<T, NB, true, false>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+        if (op == 1) return launch_fused<T, NB, false, true>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+        return launch_fused<T, NB, true, true>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+    }
+    if (op == 0) return launch_level<T, NB, true, false>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+    if (op == 1) return launch_level<T, NB, false, true>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+    return launch_level<T, NB, true, true>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+}
+
+
+#if defined(BTD_T) && defined(BTD_NB)
+template btd_status run_typed<BTD_T, BTD_NB>(const btd_plan *, int, const void *, const void *, const void *,
+                                             void *, void *, void *, int32_t *, int64_t, int64_t, cudaStream_t);
+#endif
+}  // namespace btd

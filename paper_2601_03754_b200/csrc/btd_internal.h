@@ -1,0 +1,47 @@
+// btd_internal.h -- plan structure and typed-launcher declarations shared by btd.cu and btd_inst.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/btd.h"
+#include "btd_kernels.cuh"
+
+struct btd_plan {
+    int64_t N, n, batch, m;
+    btd_dtype dtype;
+    int L;
+    int NB;        // compiled block size
+    int variant;   // BTD_VARIANT_FUSED / BTD_VARIANT_LEVEL
+    size_t smem_fs, smem_f, smem_s;  // fused smem bytes: factor+solve, factor, solve
+    btd::Geo geo;
+};
+
+
+namespace btd {
+btd_status record_cuda_error(cudaError_t e);
+
+template <int NB>
+struct TeamShape {
+    static constexpr int TS = NB <= 1 ? 1 : NB <= 2 ? 2 : NB <= 4 ? 4 : NB <= 8 ? 8 : NB <= 16 ? 16 : 32;
+    static constexpr int NT = 128 / TS;  // teams per CTA, fused kernel
+};
+
+template <typename T, int NB>
+struct LevelShape {
+    static constexpr int TS = TeamShape<NB>::TS;
+    static constexpr int BYTES = LevelSmem<T, NB>::TSTR * (int)sizeof(T);
+    static constexpr int CAP = 24 * 1024 / BYTES;
+    static constexpr int NT = CAP < 1 ? 1 : (CAP < 128 / TS ? CAP : 128 / TS);
+};
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+template <typename T, int NB>
+size_t fused_bytes(const btd_plan *p, bool fact, bool solve) {
+    return FusedSmem<T, NB, TeamShape<NB>::NT>::bytes((int)p->N, (int)p->m, fact, solve);
+}
+
+// Defined in btd_inst.cu, explicitly instantiated once per (T, NB) translation unit.
+template <typename T, int NB>
+btd_status run_typed(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
+                     void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st);
+}  // namespace btd

@@ -1,0 +1,92 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads, exports every symbol that
+include/btd.h declares, and the plan's symbolic analysis (a0) agrees with the oracle's plain
+definitions of P_inf, level counts and the coupling-slot layout."""
+import os
+import re
+
+import pytest
+import torch
+
+import paper_2601_03754_b200 as btd
+from oracle.perm import coupling_slots, num_levels, perm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "btd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(btd_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2601_03754_b200 import build
+
+    build.build()
+
+
+def test_exports_every_declared_symbol():
+    names = _declared_symbols()
+    assert len(names) >= 15
+    L = btd.lib()
+    for name in names:
+        assert hasattr(L, name), name
+    # the binding wires every declared entry point
+    assert {s[0] for s in btd.btd.SIGNATURES} == set(names)
+
+
+def test_shared_object_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", btd.btd.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 7, 8, 9, 16, 17, 20, 33, 64, 100, 128, 256, 1000, 1024, 4096])
+def test_plan_matches_oracle_definitions(N):
+    p = btd.Plan(N, 3, 2, 1, torch.float64)
+    assert p.levels == num_levels(N)
+    slots = coupling_slots(N)
+    assert p.num_coupling_blocks == len(slots)
+    for lev in range(1, p.levels + 2):
+        assert p.level_offset(lev) == sum(1 for s in slots if s[0] < lev)
+    assert p.level_offset(0) == -1 and p.level_offset(p.levels + 2) == -1
+    assert p.permutation() == [i - 1 for i in perm(N)]
+
+
+def test_variant_selection():
+    # c5 (n=12, N=128, fp32) fits one SM's shared memory -> fused; c3 (n=32, N=1024) does not
+    assert btd.Plan(128, 12, 8192, 1, torch.float32).variant == "fused"
+    assert btd.Plan(1024, 32, 1, 1, torch.float64).variant == "level"
+    assert btd.Plan(64, 16, 1, 1, torch.float64).variant == "fused"
+    assert btd.Plan(8, 2, 1, 1, torch.float64).launches() == 1
+    p = btd.Plan(1024, 32, 1, 1, torch.float64)
+    assert p.launches("factor_solve") == 1 + 2 * p.levels
+    with pytest.raises(btd.BtdError):
+        btd.Plan(4096, 32, 1, 1, torch.float64, variant="fused")
+
+
+@pytest.mark.parametrize("args", [(0, 4, 1, 1), (4, 0, 1, 1), (4, 4, 0, 1), (4, 4, 1, 0)])
+def test_plan_rejects_bad_sizes(args):
+    with pytest.raises(btd.BtdError):
+        btd.Plan(*args, dtype=torch.float32)
+
+
+def test_unsupported_block_size():
+    with pytest.raises(btd.BtdError):
+        btd.Plan(8, 200, 1, 1, torch.float64)
+
+
+def test_cpu_tensors_are_rejected():
+    """No CPU fallback: host tensors are refused before any launch."""
+    D = torch.eye(2, dtype=torch.float64).expand(1, 4, 2, 2).contiguous()
+    E = torch.zeros(1, 3, 2, 2, dtype=torch.float64)
+    with pytest.raises(btd.BtdError):
+        btd.factor(D, E)
+
+
+def test_status_strings():
+    L = btd.lib()
+    assert L.btd_status_string(0) == b"BTD_OK"
+    assert b"invalid" in L.btd_status_string(1)
