@@ -89,6 +89,9 @@ class Problem:
     b: torch.Tensor
     xstar: torch.Tensor | None
 
+    def __post_init__(self):
+        self.D, self.E, self.b = self.D.contiguous(), self.E.contiguous(), self.b.contiguous()
+
     @property
     def batch(self) -> int:
         return self.D.shape[0]

@@ -145,25 +145,25 @@ int64_t btd_plan_smem_bytes(const btd_plan *p) {
 
 btd_status btd_factor(const btd_plan *p, const void *D, const void *E, void *Dhat, void *C, int32_t *info,
                       void *stream) {
-    if (!p || !D || !Dhat || !C || !info || (p->N > 1 && !E)) return BTD_EINVAL;
+    if (!p || !D || !Dhat || (!C && p->geo.nC > 0) || !info || (p->N > 1 && !E)) return BTD_EINVAL;
     return run(p, 0, D, E, nullptr, Dhat, C, nullptr, info, 0, p->batch, stream);
 }
 
 btd_status btd_solve(const btd_plan *p, const void *Dhat, const void *C, const void *b, void *x, void *stream) {
-    if (!p || !Dhat || !C || !b || !x) return BTD_EINVAL;
+    if (!p || !Dhat || (!C && p->geo.nC > 0) || !b || !x) return BTD_EINVAL;
     return run(p, 1, nullptr, nullptr, b, (void *)Dhat, (void *)C, x, nullptr, 0, p->batch, stream);
 }
 
 btd_status btd_factor_solve(const btd_plan *p, const void *D, const void *E, const void *b, void *Dhat, void *C,
                             void *x, int32_t *info, void *stream) {
-    if (!p || !D || !b || !Dhat || !C || !x || !info || (p->N > 1 && !E)) return BTD_EINVAL;
+    if (!p || !D || !b || !Dhat || (!C && p->geo.nC > 0) || !x || !info || (p->N > 1 && !E)) return BTD_EINVAL;
     return run(p, 2, D, E, b, Dhat, C, x, info, 0, p->batch, stream);
 }
 
 btd_status btd_factor_solve_host(const btd_plan *p, const void *hD, const void *hE, const void *hb, void *hDhat,
                                  void *hC, void *hx, int32_t *hinfo, void *dD, void *dE, void *db, void *dDhat,
                                  void *dC, void *dx, int32_t *dinfo, int32_t chunks, void *stream) {
-    if (!p || !hD || !hb || !hDhat || !hC || !hx || !hinfo || !dD || !db || !dDhat || !dC || !dx || !dinfo ||
+    if (!p || !hD || !hb || !hDhat || ((!hC || !dC) && p->geo.nC > 0) || !hx || !hinfo || !dD || !db || !dDhat || !dx || !dinfo ||
         chunks < 1)
         return BTD_EINVAL;
     if (p->N > 1 && (!hE || !dE)) return BTD_EINVAL;

@@ -11,11 +11,11 @@ static btd_status launch_fused(const btd_plan *p, const T *D, const T *E, const 
     constexpr int TS = TeamShape<NB>::TS, NT = TeamShape<NB>::NT;
     auto kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE>;
     const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+    static size_t attr_bytes = 0;  // per instantiation: opt in to > 48 KB dynamic smem once per size
+    if (smem > 48 * 1024 && smem > attr_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e);
-        attr_set = true;
+        attr_bytes = smem;
     }
     for (int64_t s0 = 0; s0 < count; s0 += (1ll << 30)) {
         const int64_t cnt = (count - s0) < (1ll << 30) ? (count - s0) : (1ll << 30);

@@ -33,7 +33,7 @@ struct LevelShape {
     static constexpr int NT = CAP < 1 ? 1 : (CAP < 128 / TS ? CAP : 128 / TS);
 };
 
-constexpr size_t kMaxSmem = 227 * 1024;
+constexpr size_t kMaxSmem = 227 * 1024 - 64;  // minus the kernel's static shared bytes
 
 template <typename T, int NB>
 size_t fused_bytes(const btd_plan *p, bool fact, bool solve) {
