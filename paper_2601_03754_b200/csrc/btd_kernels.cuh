@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
             }
             // -- a6: y_c <- D^^{-1} y_c ; y_{c+s} -= C_r y_c
             if (SOLVE) {
-                const T inv_r = T(1) / pick<T, NB>(dl, r);
+                __syncwarp();
+                const T inv_r = rv ? sLt[r * LD + r] : T(1);  // 1/L[r][r] (team_put_Lt)
                 for (int q = 0; q < m; ++q) {
                     T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                     T yv = (act && rv) ? yc[r] : T(0);
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
                 g_load_col<T, NB>(lc, Dh + (size_t)(c - 1) * nn, n, r, act, true);
                 g_load_col<T, NB>(crc, Cs + cslot(g, l, c / s) * nn, n, r, hasR, false);
                 g_load_row<T, NB>(clr, Cs + cslot(g, l, c / s - 1) * nn, n, r, hasL, false);
-                const T inv_r = T(1) / pick<T, NB>(lc, r);
+                const T inv_r = (act && r < n) ? T(1) / Dh[(size_t)(c - 1) * nn + (size_t)r * n + r] : T(1);
                 for (int q = 0; q < m; ++q) {
                     T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                     T v = (act && rv) ? yc[r] : T(0);
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, co
     g_load_col<T, NB>(lc, Dh + (size_t)(c - 1) * nn, n, r, act, true);
     g_load_col<T, NB>(crc, Cs + cslot(g, l, c / s) * nn, n, r, hasR, false);
     g_load_row<T, NB>(clr, Cs + cslot(g, l, c / s - 1) * nn, n, r, hasL, false);
-    const T inv_r = T(1) / pick<T, NB>(lc, r);
+    const T inv_r = (act && r < n) ? T(1) / Dh[(size_t)(c - 1) * nn + (size_t)r * n + r] : T(1);
     for (int q = 0; q < m; ++q) {
         if (rv) {
             sx[team][0][r] = (hasR && r < n) ? xs[((size_t)(c + s - 1) * n + r) * m + q] : T(0);

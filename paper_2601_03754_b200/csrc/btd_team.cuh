@@ -101,7 +101,10 @@ __device__ __forceinline__ void g_load_row(T (&v)[NB], const T *blk, int n, int 
             vload<T, NB>(v, blk + (size_t)r * NB);
         } else {
 #pragma unroll
-            for (int j = 0; j < NB; ++j) v[j] = (j < n) ? blk[(size_t)r * n + j] : T(0);
+            for (int j = 0; j < NB; ++j) {
+                const T t = blk[(size_t)r * n + (j < n ? j : n - 1)];
+                v[j] = (j < n) ? t : T(0);
+            }
         }
     } else {
 #pragma unroll
@@ -113,12 +116,13 @@ __device__ __forceinline__ void g_load_row(T (&v)[NB], const T *blk, int n, int 
 template <typename T, int NB>
 __device__ __forceinline__ void g_load_col(T (&v)[NB], const T *blk, int n, int r, bool act,
                                            bool identity_pad) {
+    const bool on = act && r < n;
+    const int rc = on ? r : 0;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        if (act && r < n)
-            v[i] = (i < n) ? blk[(size_t)i * n + r] : T(0);
-        else
-            v[i] = (identity_pad && i == r) ? T(1) : T(0);
+        T t = T(0);
+        if (on) t = blk[(size_t)(i < n ? i : n - 1) * n + rc];
+        v[i] = on ? ((i < n) ? t : T(0)) : ((identity_pad && i == r) ? T(1) : T(0));
     }
 }
 
@@ -128,18 +132,20 @@ __device__ __forceinline__ void g_store_row(T *blk, const T (&v)[NB], int n, int
     if ((NB * (int)sizeof(T)) % 16 == 0 && n == NB) {
         vstore<T, NB>(blk + (size_t)r * NB, v);
     } else {
+        const unsigned long long msk = (n >= 64) ? ~0ull : ((1ull << n) - 1);
 #pragma unroll
         for (int j = 0; j < NB; ++j)
-            if (j < n) blk[(size_t)r * n + j] = v[j];
+            if ((msk >> j) & 1ull) blk[(size_t)r * n + j] = v[j];
     }
 }
 
 template <typename T, int NB>
 __device__ __forceinline__ void g_store_col(T *blk, const T (&v)[NB], int n, int r, bool act) {
     if (!(act && r < n)) return;
+    const unsigned long long msk = (n >= 64) ? ~0ull : ((1ull << n) - 1);
 #pragma unroll
     for (int i = 0; i < NB; ++i)
-        if (i < n) blk[(size_t)i * n + r] = v[i];
+        if ((msk >> i) & 1ull) blk[(size_t)i * n + r] = v[i];
 }
 
 // ------------------------------------------------------------------ team numerics
@@ -149,26 +155,26 @@ __device__ __forceinline__ void g_store_col(T *blk, const T (&v)[NB], int n, int
 // return value is uniform over the team. Entries above the diagonal are set to 0.
 template <typename T, int NB>
 __device__ __forceinline__ int team_potrf(T (&a)[NB], int r, int base) {
+    // Branch-free on the lane row r: every lane updates its whole register row (entries above
+    // the diagonal become don't-care values and are cleared at the end). Data-dependent
+    // predicates on r would let the compiler re-roll the unrolled loops into a runtime-bounded
+    // loop and demote a[] to local memory.
     int bad = -1;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
         const T akk = __shfl_sync(kFull, a[k], base + k);
-        if (!(akk > T(0)) && bad < 0) bad = k;
+        bad = (!(akk > T(0)) && bad < 0) ? k : bad;
         const T d = sqrt(akk);
         const T inv = T(1) / d;
-        if (r == k)
-            a[k] = d;
-        else if (r > k)
-            a[k] *= inv;
+        a[k] = (r == k) ? d : a[k] * inv;
 #pragma unroll
         for (int j = k + 1; j < NB; ++j) {
             const T ljk = __shfl_sync(kFull, a[k], base + j);
-            if (r >= j) a[j] = fma(-a[k], ljk, a[j]);
+            a[j] = fma(-a[k], ljk, a[j]);
         }
     }
 #pragma unroll
-    for (int j = 0; j < NB; ++j)
-        if (j > r) a[j] = T(0);
+    for (int j = 0; j < NB; ++j) a[j] = (j > r) ? T(0) : a[j];
     return bad;
 }
 
@@ -179,12 +185,8 @@ __device__ __forceinline__ void team_put_Lt(T *sLt, const T (&a)[NB], int r) {
     if (r >= NB) return;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-        if (k < r)
-            sLt[k * LD + r] = a[k];
-        else if (k == r)
-            sLt[k * LD + r] = T(1) / a[k];
-        else
-            sLt[k * LD + r] = T(0);
+        const T v = (k < r) ? a[k] : ((k == r) ? T(1) / a[k] : T(0));
+        sLt[k * LD + r] = v;
     }
 }
 
@@ -240,10 +242,8 @@ __device__ __forceinline__ T team_fwd(T y, const T (&a)[NB], T inv_r, int r, int
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
         const T xk = __shfl_sync(kFull, y * inv_r, base + k);
-        if (r == k)
-            y = xk;
-        else if (r > k)
-            y = fma(-a[k], xk, y);
+        const T upd = fma(-a[k], xk, y);
+        y = (r == k) ? xk : ((r > k) ? upd : y);
     }
     return y;
 }
@@ -255,10 +255,8 @@ __device__ __forceinline__ T team_bwd(T v, const T (&lc)[NB], T inv_r, int r, in
 #pragma unroll
     for (int k = NB - 1; k >= 0; --k) {
         const T xk = __shfl_sync(kFull, v * inv_r, base + k);
-        if (r == k)
-            v = xk;
-        else if (r < k)
-            v = fma(-lc[k], xk, v);
+        const T upd = fma(-lc[k], xk, v);
+        v = (r == k) ? xk : ((r < k) ? upd : v);
     }
     return v;
 }
