@@ -5,11 +5,11 @@
 namespace btd {
 static btd_status cuda_fail(cudaError_t e) { return record_cuda_error(e); }
 
-template <typename T, int NB, bool FACT, bool SOLVE>
-static btd_status launch_fused(const btd_plan *p, const T *D, const T *E, const T *b, T *Dhat, T *C, T *x,
-                               int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
-    constexpr int TS = TeamShape<NB>::TS, NT = TeamShape<NB>::NT;
-    auto kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE>;
+template <typename T, int NB, bool FACT, bool SOLVE, int MR>
+static btd_status launch_fused_mr(const btd_plan *p, const T *D, const T *E, const T *b, T *Dhat, T *C, T *x,
+                                  int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    constexpr int TS = FusedCfg<T, NB>::TS, NT = FusedCfg<T, NB>::NT;
+    auto kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
     const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
     static size_t attr_bytes = 0;  // per instantiation: opt in to > 48 KB dynamic smem once per size
     if (smem > 48 * 1024 && smem > attr_bytes) {
@@ -24,6 +24,15 @@ static btd_status launch_fused(const btd_plan *p, const T *D, const T *E, const 
         if (e != cudaSuccess) return cuda_fail(e);
     }
     return BTD_OK;
+}
+
+template <typename T, int NB, bool FACT, bool SOLVE>
+static btd_status launch_fused(const btd_plan *p, const T *D, const T *E, const T *b, T *Dhat, T *C, T *x,
+                               int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    if constexpr (SOLVE) {
+        if (p->m == 1) return launch_fused_mr<T, NB, FACT, SOLVE, 1>(p, D, E, b, Dhat, C, x, info, sys0, count, st);
+    }
+    return launch_fused_mr<T, NB, FACT, SOLVE, 0>(p, D, E, b, Dhat, C, x, info, sys0, count, st);
 }
 
 template <typename T, int NB, bool FACT, bool SOLVE>

@@ -40,32 +40,46 @@ __device__ __forceinline__ long long cslot(const Geo &g, int l, int k) { return 
 // Shared memory (elements of T):
 //   slots   N * BLK            (FACT only)
 //   Y       N * m * LD         (SOLVE only; y then x, one padded row per block and rhs)
-//   scratch NT * TSTR          (4 blocks per team, TSTR padded by 64 B against bank conflicts)
+//   scratch NT * TSTR          (3 blocks per team: sLt (later reused as sCl), sCr, sClT;
+//                               TSTR padded by 64 B so the two teams of a warp hit different banks)
 template <typename T, int NB, int NT>
 struct FusedSmem {
     static constexpr int LD = Dims<T, NB>::LD;
     static constexpr int BLK = Dims<T, NB>::BLK;
-    static constexpr int TSTR = 4 * BLK + 64 / (int)sizeof(T);
+    static constexpr int TSTR = 3 * BLK + 64 / (int)sizeof(T);
     static __host__ __device__ size_t bytes(int N, int m, bool fact, bool solve) {
         size_t e = (fact ? (size_t)N * BLK : 0) + (solve ? (size_t)N * m * LD : 0) + (size_t)NT * TSTR;
         return e * sizeof(T);
     }
 };
 
-template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE>
-__global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__ D, const T *__restrict__ E,
-                                                          const T *__restrict__ bvec, T *Dhat, T *C, T *x,
-                                                          int32_t *info, Geo g, int sys0) {
+// Launch shape of the fused kernel for block size NB: team width TS, CTA threads, min CTAs/SM.
+template <typename T, int NB>
+struct FusedCfg {
+    static constexpr int TS = NB <= 1 ? 1 : NB <= 2 ? 2 : NB <= 4 ? 4 : NB <= 8 ? 8 : NB <= 16 ? 16 : 32;
+    static constexpr int LIM = sizeof(T) == 4 ? 16 : 8;  // register rows per lane that fit 128 regs
+    static constexpr int THREADS = NB <= LIM ? 256 : 128;
+    static constexpr int NT = THREADS / TS;
+    static constexpr int MINB = NB <= LIM ? 2 : 1;
+};
+
+// MR = number of right-hand sides if fixed at compile time (1), 0 = runtime g.m.
+template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE, int MR>
+__global__ void __launch_bounds__(NT *TS, FusedCfg<T, NB>::MINB)
+    btd_fused_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C,
+                     T *x, int32_t *info, Geo g, int sys0) {
     using S = FusedSmem<T, NB, NT>;
     constexpr int LD = S::LD, BLK = S::BLK;
+    constexpr int TPW = 32 / TS;  // teams per warp
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *smem = reinterpret_cast<T *>(smem_raw);
     T *slots = smem;
     T *Y = smem + (FACT ? (size_t)g.N * BLK : 0);
-    T *scr = Y + (SOLVE ? (size_t)g.N * g.m * LD : 0);
     __shared__ unsigned s_fail;
 
-    const int N = g.N, n = g.n, m = g.m;
+    const int N = g.N, n = g.n;
+    const int m = MR > 0 ? MR : g.m;
+    T *scr = Y + (SOLVE ? (size_t)N * m * LD : 0);
     const long long sys = (long long)blockIdx.x + sys0;
     const size_t nn = (size_t)n * n;
     const T *Ds = D ? D + sys * N * nn : nullptr;
@@ -75,14 +89,16 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
+    const int warp = tid >> 5;
     const int team = tid / TS;
     const int r = lane % TS;
     const int base = lane - r;
     const bool rv = r < NB;  // lane owns a (possibly padded) row
+    const int rr = rv ? r : 0;
     T *sLt = scr + (size_t)team * S::TSTR;
+    T *sCl = sLt;  // reuses sLt once both TRSMs are done
     T *sCr = sLt + BLK;
     T *sClT = sCr + BLK;
-    T *sCl = sClT + BLK;
 
     if (tid == 0) s_fail = 0xffffffffu;
     // ---- a1: load.  slots <- D (padded with identity); Y <- b.
@@ -100,11 +116,11 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
             }
         } else {
             for (size_t q = tid; q < (size_t)N * BLK; q += blockDim.x) {
-                const int i = (int)(q / BLK), rr = (int)((q % BLK) / LD), cc = (int)(q % LD);
+                const int i = (int)(q / BLK), r2 = (int)((q % BLK) / LD), c2 = (int)(q % LD);
                 T v = T(0);
-                if (rr < n && cc < n)
-                    v = Ds[(size_t)i * nn + (size_t)rr * n + cc];
-                else if (rr == cc)
+                if (r2 < n && c2 < n)
+                    v = Ds[(size_t)i * nn + (size_t)r2 * n + c2];
+                else if (r2 == c2)
                     v = T(1);
                 slots[q] = v;
             }
@@ -114,113 +130,123 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
         const T *bs = bvec + sys * (size_t)N * n * m;
         for (size_t q = tid; q < (size_t)N * m * LD; q += blockDim.x) {
             const int i = (int)(q / ((size_t)m * LD)), rem = (int)(q % ((size_t)m * LD));
-            const int qq = rem / LD, rr = rem % LD;
-            Y[q] = (rr < n) ? bs[((size_t)i * n + rr) * m + qq] : T(0);
+            const int qq = rem / LD, r2 = rem % LD;
+            Y[q] = (r2 < n) ? bs[((size_t)i * n + r2) * m + qq] : T(0);
         }
     }
     __syncthreads();
 
-    // ---- levels l = 1..L (stride s): a2-a7 forward part
+    // ---- levels l = 1..L (stride s): a2-a6
     for (int l = 1; l <= g.L; ++l) {
         const int s = 1 << (l - 1);
         const int ncols = ((N / s) + 1) / 2;
+        const long long offL = g.off[l - 1];
+        const long long offN = g.off[l];
         for (int j0 = 0; j0 < ncols; j0 += NT) {
             const int j = j0 + team;
+            const bool wact = j0 + warp * TPW < ncols;  // warp has at least one active team
             const bool act = j < ncols;
             const int c = s * (2 * j + 1);
             const bool hasL = act && c > s;
             const bool hasR = act && (c + s <= N);
-
-            // -- a3: D~_c -> D^_c
-            T dl[NB];
-            if (FACT) {
-                if (act && rv)
-                    vload<T, NB>(dl, slots + (size_t)(c - 1) * BLK + r * LD);
-                else {
+            T cl[NB];
+            if (wact) {
+                // -- a3: D~_c -> D^_c
+                T dl[NB];
+                if (FACT) {
+                    vload<T, NB>(dl, slots + (size_t)((act ? c : 1) - 1) * BLK + rr * LD);
+                    if (!(act && rv)) {
 #pragma unroll
-                    for (int q = 0; q < NB; ++q) dl[q] = (q == r) ? T(1) : T(0);
-                }
-                const int bad = team_potrf<T, NB>(dl, r, base);
-                if (act && bad >= 0 && r == 0) atomicMin(&s_fail, fail_key(c));
-                g_store_row<T, NB>(Dh + (size_t)(c - 1) * nn, dl, n, r, act);
-            } else {
-                g_load_row<T, NB>(dl, Dh + (size_t)(c - 1) * nn, n, r, act, true);
-            }
-            team_put_Lt<T, NB>(sLt, dl, r);
-
-            // -- a4: couplings. cr = row r of the right coupling, cl = column r of the left one.
-            T cr[NB], cl[NB];
-            if (FACT) {
-                if (l == 1) {
-                    g_load_row<T, NB>(cr, Es + (size_t)(c - 1) * nn, n, r, hasR, false);  // E_c   = (c+1, c)
-                    g_load_col<T, NB>(cl, Es + (size_t)(c - 2) * nn, n, r, hasL, false);  // E_c-1 = (c, c-1)
-                } else {
-                    if (hasR && rv)
-                        vload<T, NB>(cr, slots + (size_t)(c + s / 2 - 1) * BLK + r * LD);
-                    else {
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) cr[q] = T(0);
+                        for (int q = 0; q < NB; ++q) dl[q] = (q == r) ? T(1) : T(0);
                     }
-#pragma unroll
-                    for (int q = 0; q < NB; ++q)
-                        cl[q] = (hasL && rv) ? slots[(size_t)(c - s / 2 - 1) * BLK + q * LD + r] : T(0);
+                    const int bad = team_potrf<T, NB>(dl, r, base);
+                    if (act && bad >= 0 && r == 0) atomicMin(&s_fail, fail_key(c));
+                    g_store_row<T, NB>(Dh + (size_t)(c - 1) * nn, dl, n, r, act);
+                } else {
+                    g_load_row<T, NB>(dl, Dh + (size_t)(c - 1) * nn, n, r, act, true);
                 }
-                __syncwarp();
-                tri_solve<T, NB>(cr, sLt);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
-                tri_solve<T, NB>(cl, sLt);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
-                g_store_row<T, NB>(Cs + cslot(g, l, c / s) * nn, cr, n, r, hasR);
-                g_store_col<T, NB>(Cs + cslot(g, l, c / s - 1) * nn, cl, n, r, hasL);
-            } else {
-                g_load_row<T, NB>(cr, Cs + cslot(g, l, c / s) * nn, n, r, hasR, false);
-                g_load_col<T, NB>(cl, Cs + cslot(g, l, c / s - 1) * nn, n, r, hasL, false);
-            }
-            if (rv) {
-                vstore<T, NB>(sCr + r * LD, cr);
-                vstore<T, NB>(sClT + r * LD, cl);
-#pragma unroll
-                for (int q = 0; q < NB; ++q) sCl[q * LD + r] = cl[q];
-            }
-            __syncwarp();
+                team_put_Lt<T, NB>(sLt, dl, r);
 
-            if (FACT) {
-                // -- a5: fill  C_{l+1,(c-s)/2s} = -C_r C_l  -> slot[c] (column c's D~ is consumed)
-                if (hasL && hasR && rv) {
-                    T f[NB];
+                // -- a4: couplings. cr = row r of the right coupling, cl = column r of the left one.
+                T cr[NB];
+                if (FACT) {
+                    if (l == 1) {
+                        g_load_row<T, NB>(cr, Es + (size_t)(c - 1) * nn, n, r, hasR, false);  // E_c   = (c+1, c)
+                        g_load_col<T, NB>(cl, Es + (size_t)(c - 2) * nn, n, r, hasL, false);  // E_c-1 = (c, c-1)
+                    } else {
+                        vload<T, NB>(cr, slots + (size_t)((hasR ? c + s / 2 : 1) - 1) * BLK + rr * LD);
+                        const T *pl = slots + (size_t)((hasL ? c - s / 2 : 1) - 1) * BLK + rr;
 #pragma unroll
-                    for (int q = 0; q < NB; ++q) f[q] = T(0);
-                    rowmat_sub<T, NB>(f, cr, sCl);
-                    vstore<T, NB>(slots + (size_t)(c - 1) * BLK + r * LD, f);
+                        for (int q = 0; q < NB; ++q) cl[q] = pl[q * LD];
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) {
+                            cr[q] = (hasR && rv) ? cr[q] : T(0);
+                            cl[q] = (hasL && rv) ? cl[q] : T(0);
+                        }
+                    }
+                    __syncwarp();
+                    tri_solve<T, NB>(cr, sLt);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
+                    tri_solve<T, NB>(cl, sLt);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
+                    g_store_row<T, NB>(Cs + (offL + c / s - 1) * nn, cr, n, r, hasR);
+                    g_store_col<T, NB>(Cs + (offL + c / s - 2) * nn, cl, n, r, hasL);
+                } else {
+                    g_load_row<T, NB>(cr, Cs + (offL + c / s - 1) * nn, n, r, hasR, false);
+                    g_load_col<T, NB>(cl, Cs + (offL + c / s - 2) * nn, n, r, hasL, false);
                 }
-                // -- a2 (right): D~_{c+s} -= C_r C_r^T
-                if (hasR && rv) {
-                    T acc[NB];
-                    T *p = slots + (size_t)(c + s - 1) * BLK + r * LD;
-                    vload<T, NB>(acc, p);
-                    rowdot_sub<T, NB>(acc, cr, sCr);
-                    vstore<T, NB>(p, acc);
+                T inv_r = T(1);
+                if (SOLVE) {
+                    __syncwarp();
+                    inv_r = sLt[rr * LD + rr];  // 1/L[r][r] (team_put_Lt)
                 }
-            }
-            // -- a6: y_c <- D^^{-1} y_c ; y_{c+s} -= C_r y_c
-            if (SOLVE) {
+                __syncwarp();  // sLt is dead from here on; sCl reuses it
+                if (rv) {
+                    vstore<T, NB>(sCr + r * LD, cr);
+                    vstore<T, NB>(sClT + r * LD, cl);
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) sCl[q * LD + r] = cl[q];
+                }
                 __syncwarp();
-                const T inv_r = rv ? sLt[r * LD + r] : T(1);  // 1/L[r][r] (team_put_Lt)
-                for (int q = 0; q < m; ++q) {
-                    T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
-                    T yv = (act && rv) ? yc[r] : T(0);
-                    yv = team_fwd<T, NB>(yv, dl, inv_r, r, base);
-                    if (act && rv) yc[r] = yv;
+
+                if (FACT) {
+                    // -- a5: fill  C_{l+1,(c-s)/2s} = -C_r C_l  -> slot[c] (column c's D~ is consumed)
+                    if (hasL && hasR && rv) {
+                        T f[NB];
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) f[q] = T(0);
+                        rowmat_sub<T, NB>(f, cr, sCl);
+                        vstore<T, NB>(slots + (size_t)(c - 1) * BLK + r * LD, f);
+                    }
+                    // -- a2 (right): D~_{c+s} -= C_r C_r^T
+                    if (hasR && rv) {
+                        T acc[NB];
+                        T *p = slots + (size_t)(c + s - 1) * BLK + r * LD;
+                        vload<T, NB>(acc, p);
+                        rowdot_sub<T, NB>(acc, cr, sCr);
+                        vstore<T, NB>(p, acc);
+                    }
                 }
-                __syncwarp();
-                if (hasR && rv) {
+                (void)offN;
+                // -- a6: y_c <- D^^{-1} y_c ; y_{c+s} -= C_r y_c
+                if (SOLVE) {
                     for (int q = 0; q < m; ++q) {
-                        const T d = dot<T, NB>(cr, Y + ((size_t)(c - 1) * m + q) * LD);
-                        Y[((size_t)(c + s - 1) * m + q) * LD + r] -= d;
+                        T *yc = Y + ((size_t)((act ? c : 1) - 1) * m + q) * LD;
+                        T yv = yc[rr];
+                        yv = (act && rv) ? yv : T(0);
+                        yv = team_fwd<T, NB>(yv, dl, inv_r, r, base);
+                        if (act && rv) yc[r] = yv;
+                    }
+                    __syncwarp();
+                    if (hasR && rv) {
+                        for (int q = 0; q < m; ++q) {
+                            const T d = dot<T, NB>(cr, Y + ((size_t)(c - 1) * m + q) * LD);
+                            Y[((size_t)(c + s - 1) * m + q) * LD + r] -= d;
+                        }
                     }
                 }
             }
             __syncthreads();
             // ---- phase Y: left pushes (deferred left-looking part of Alg. 4, l.7/l.9)
-            if (hasL && rv) {
+            if (wact && hasL && rv) {
                 if (FACT) {
                     T acc[NB];
                     T *p = slots + (size_t)(c - s - 1) * BLK + r * LD;
@@ -244,7 +270,9 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
         for (int l = g.L; l >= 1; --l) {
             const int s = 1 << (l - 1);
             const int ncols = ((N / s) + 1) / 2;
+            const long long offL = g.off[l - 1];
             for (int j0 = 0; j0 < ncols; j0 += NT) {
+                if (j0 + warp * TPW >= ncols) continue;  // warp-uniform
                 const int j = j0 + team;
                 const bool act = j < ncols;
                 const int c = s * (2 * j + 1);
@@ -252,14 +280,18 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
                 const bool hasR = act && (c + s <= N);
                 T lc[NB], crc[NB], clr[NB];
                 g_load_col<T, NB>(lc, Dh + (size_t)(c - 1) * nn, n, r, act, true);
-                g_load_col<T, NB>(crc, Cs + cslot(g, l, c / s) * nn, n, r, hasR, false);
-                g_load_row<T, NB>(clr, Cs + cslot(g, l, c / s - 1) * nn, n, r, hasL, false);
-                const T inv_r = (act && r < n) ? T(1) / Dh[(size_t)(c - 1) * nn + (size_t)r * n + r] : T(1);
+                g_load_col<T, NB>(crc, Cs + (offL + c / s - 1) * nn, n, r, hasR, false);
+                g_load_row<T, NB>(clr, Cs + (offL + c / s - 2) * nn, n, r, hasL, false);
+                const T dg = Dh[(size_t)((act ? c : 1) - 1) * nn + (size_t)(r < n ? r : 0) * (n + 1)];
+                const T inv_r = (act && r < n) ? T(1) / dg : T(1);
                 for (int q = 0; q < m; ++q) {
-                    T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
-                    T v = (act && rv) ? yc[r] : T(0);
-                    if (hasR) v -= dot<T, NB>(crc, Y + ((size_t)(c + s - 1) * m + q) * LD);
-                    if (hasL) v -= dot<T, NB>(clr, Y + ((size_t)(c - s - 1) * m + q) * LD);
+                    T *yc = Y + ((size_t)((act ? c : 1) - 1) * m + q) * LD;
+                    T v = yc[rr];
+                    v = (act && rv) ? v : T(0);
+                    const T a = dot<T, NB>(crc, Y + ((size_t)((hasR ? c + s : 1) - 1) * m + q) * LD);
+                    const T b2 = dot<T, NB>(clr, Y + ((size_t)((hasL ? c - s : 1) - 1) * m + q) * LD);
+                    v -= hasR ? a : T(0);
+                    v -= hasL ? b2 : T(0);
                     v = team_bwd<T, NB>(v, lc, inv_r, r, base);
                     if (act && rv) yc[r] = v;
                 }
@@ -269,12 +301,13 @@ __global__ void __launch_bounds__(NT *TS) btd_fused_kernel(const T *__restrict__
         T *xs = x + sys * (size_t)N * n * m;
         for (size_t q = tid; q < (size_t)N * n * m; q += blockDim.x) {
             const int i = (int)(q / ((size_t)n * m)), rem = (int)(q % ((size_t)n * m));
-            const int rr = rem / m, qq = rem % m;
-            xs[q] = Y[((size_t)i * m + qq) * LD + rr];
+            const int r2 = rem / m, qq = rem % m;
+            xs[q] = Y[((size_t)i * m + qq) * LD + r2];
         }
     }
     if (FACT && tid == 0) info[sys] = (s_fail == 0xffffffffu) ? 0 : (int)(s_fail & ((1u << 25) - 1));
 }
+
 
 // ============================================================================ LEVEL
 //
