@@ -8,8 +8,14 @@ static btd_status cuda_fail(cudaError_t e) { return record_cuda_error(e); }
 template <typename T, int NB, bool FACT, bool SOLVE, int MR>
 static btd_status launch_fused_mr(const btd_plan *p, const T *D, const T *E, const T *b, T *Dhat, T *C, T *x,
                                   int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
-    constexpr int TS = FusedCfg<T, NB>::TS, NT = FusedCfg<T, NB>::NT;
-    auto kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
+    constexpr bool R = FusedRCfg<T, NB>::OK;
+    constexpr int TS = R ? FusedRCfg<T, NB>::TS : FusedCfg<T, NB>::TS;
+    constexpr int NT = R ? FusedRCfg<T, NB>::NT : FusedCfg<T, NB>::NT;
+    void (*kern)(const T *, const T *, const T *, T *, T *, T *, int32_t *, Geo, int);
+    if constexpr (R)
+        kern = btd_fused_r_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
+    else
+        kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
     const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
     static size_t attr_bytes = 0;  // per instantiation: opt in to > 48 KB dynamic smem once per size
     if (smem > 48 * 1024 && smem > attr_bytes) {

@@ -37,6 +37,7 @@ constexpr size_t kMaxSmem = 227 * 1024 - 64;  // minus the kernel's static share
 
 template <typename T, int NB>
 size_t fused_bytes(const btd_plan *p, bool fact, bool solve) {
+    if (FusedRCfg<T, NB>::OK) return FusedRCfg<T, NB>::bytes((int)p->N, (int)p->m, fact, solve);
     return FusedSmem<T, NB, FusedCfg<T, NB>::NT>::bytes((int)p->N, (int)p->m, fact, solve);
 }
 

@@ -1,7 +1,7 @@
 // btd_kernels.cuh -- the level kernels of the multi-stage block-tridiagonal Cholesky.
 //
-// Two realisations of Algorithm 4 (factor) + Algorithm 6 (solve,
-// PAPER.md:596-619), both built from the team primitives of btd_team.cuh:
+// Realisations of Algorithm 4 (factor) + Algorithm 6 (solve),
+// all built from the team primitives of btd_team.cuh:
 //
 //  FUSED  one CTA per system runs every level and both sweeps in one launch. The working
 //         blocks live in shared memory in one slot per original block index:
@@ -13,6 +13,14 @@
 //         to the left separator (the update Alg. 4 defers to the next level, l.7/l.9), so a
 //         separator always receives left child then right child, race-free and deterministic.
 //         L^ streams to HBM once; the backward sweep re-reads it (L2-resident).
+//         Two team layouts:
+//           FUSED-R (small blocks: fp32 n <= 12, fp64 n <= 8): TS lanes x RPL rows per lane with
+//                   RPL = NB/TS, the whole factor L^ of the column held in every lane's registers
+//                   (TRSMs and the forward/backward solves need no communication), GEMM operands
+//                   exchanged by warp shuffles -- no shared-memory scratch, so two systems fit
+//                   per SM.
+//           FUSED-S (larger blocks): one row per lane, L^ and the coupling rows staged in a
+//                   per-team shared-memory scratch and read as broadcasts.
 //
 //  LEVEL  one launch per level for factor(+forward) and one per level for the backward sweep,
 //         state in the caller's output buffers (D~ in Dhat, raw fill in its final C slot, y/x
@@ -35,73 +43,14 @@ struct Geo {
 
 __device__ __forceinline__ long long cslot(const Geo &g, int l, int k) { return g.off[l - 1] + k - 1; }
 
-// ============================================================================ FUSED
-//
-// Shared memory (elements of T):
-//   slots   N * BLK            (FACT only)
-//   Y       N * m * LD         (SOLVE only; y then x, one padded row per block and rhs)
-//   scratch NT * TSTR          (3 blocks per team: sLt (later reused as sCl), sCr, sClT;
-//                               TSTR padded by 64 B so the two teams of a warp hit different banks)
-template <typename T, int NB, int NT>
-struct FusedSmem {
-    static constexpr int LD = Dims<T, NB>::LD;
-    static constexpr int BLK = Dims<T, NB>::BLK;
-    static constexpr int TSTR = 3 * BLK + 64 / (int)sizeof(T);
-    static __host__ __device__ size_t bytes(int N, int m, bool fact, bool solve) {
-        size_t e = (fact ? (size_t)N * BLK : 0) + (solve ? (size_t)N * m * LD : 0) + (size_t)NT * TSTR;
-        return e * sizeof(T);
-    }
-};
+// ---------------------------------------------------------------------------- shared pieces
 
-// Launch shape of the fused kernel for block size NB: team width TS, CTA threads, min CTAs/SM.
-template <typename T, int NB>
-struct FusedCfg {
-    static constexpr int TS = NB <= 1 ? 1 : NB <= 2 ? 2 : NB <= 4 ? 4 : NB <= 8 ? 8 : NB <= 16 ? 16 : 32;
-    static constexpr int LIM = sizeof(T) == 4 ? 16 : 8;  // register rows per lane that fit 128 regs
-    static constexpr int THREADS = NB <= LIM ? 256 : 128;
-    static constexpr int NT = THREADS / TS;
-    static constexpr int MINB = NB <= LIM ? 2 : 1;
-};
-
-// MR = number of right-hand sides if fixed at compile time (1), 0 = runtime g.m.
-template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE, int MR>
-__global__ void __launch_bounds__(NT *TS, FusedCfg<T, NB>::MINB)
-    btd_fused_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C,
-                     T *x, int32_t *info, Geo g, int sys0) {
-    using S = FusedSmem<T, NB, NT>;
-    constexpr int LD = S::LD, BLK = S::BLK;
-    constexpr int TPW = 32 / TS;  // teams per warp
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *smem = reinterpret_cast<T *>(smem_raw);
-    T *slots = smem;
-    T *Y = smem + (FACT ? (size_t)g.N * BLK : 0);
-    __shared__ unsigned s_fail;
-
-    const int N = g.N, n = g.n;
-    const int m = MR > 0 ? MR : g.m;
-    T *scr = Y + (SOLVE ? (size_t)N * m * LD : 0);
-    const long long sys = (long long)blockIdx.x + sys0;
-    const size_t nn = (size_t)n * n;
-    const T *Ds = D ? D + sys * N * nn : nullptr;
-    const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
-    T *Dh = Dhat + sys * N * nn;
-    T *Cs = C + sys * (size_t)g.nC * nn;
-
+// slots <- D (padded with identity), Y <- b (padded rows), cooperative over the CTA.
+template <typename T, int NB, bool FACT, bool SOLVE>
+__device__ __forceinline__ void fused_load_inputs(T *slots, T *Y, const T *Ds, const T *bs, int N, int n, int m) {
+    constexpr int LD = Dims<T, NB>::LD, BLK = Dims<T, NB>::BLK;
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const int team = tid / TS;
-    const int r = lane % TS;
-    const int base = lane - r;
-    const bool rv = r < NB;  // lane owns a (possibly padded) row
-    const int rr = rv ? r : 0;
-    T *sLt = scr + (size_t)team * S::TSTR;
-    T *sCl = sLt;  // reuses sLt once both TRSMs are done
-    T *sCr = sLt + BLK;
-    T *sClT = sCr + BLK;
-
-    if (tid == 0) s_fail = 0xffffffffu;
-    // ---- a1: load.  slots <- D (padded with identity); Y <- b.
+    const size_t nn = (size_t)n * n;
     if (FACT) {
         if (n == NB && LD == NB) {
             constexpr int W = VecT<T>::W;
@@ -127,137 +76,290 @@ __global__ void __launch_bounds__(NT *TS, FusedCfg<T, NB>::MINB)
         }
     }
     if (SOLVE) {
-        const T *bs = bvec + sys * (size_t)N * n * m;
         for (size_t q = tid; q < (size_t)N * m * LD; q += blockDim.x) {
             const int i = (int)(q / ((size_t)m * LD)), rem = (int)(q % ((size_t)m * LD));
             const int qq = rem / LD, r2 = rem % LD;
             Y[q] = (r2 < n) ? bs[((size_t)i * n + r2) * m + qq] : T(0);
         }
     }
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void fused_store_x(T *xs, const T *Y, int N, int n, int m) {
+    constexpr int LD = Dims<T, NB>::LD;
+    for (size_t q = threadIdx.x; q < (size_t)N * n * m; q += blockDim.x) {
+        const int i = (int)(q / ((size_t)n * m)), rem = (int)(q % ((size_t)n * m));
+        const int r2 = rem / m, qq = rem % m;
+        xs[q] = Y[((size_t)i * m + qq) * LD + r2];
+    }
+}
+
+// v[k] of the lane's row k... select v[i] for a runtime index i without dynamic register indexing.
+template <typename T, int NB>
+__device__ __forceinline__ T select_idx(const T (&v)[NB], int i) {
+    T out = v[0];
+#pragma unroll
+    for (int k = 1; k < NB; ++k) out = (i == k) ? v[k] : out;
+    return out;
+}
+
+// ============================================================================ FUSED-R
+//
+// Shared memory (elements of T): slots N * BLK (FACT), Y N * m * LD (SOLVE). No scratch.
+template <typename T, int NB>
+struct FusedRCfg {
+    // team width: NB / TS rows per lane, every lane busy (TS divides NB and 32)
+    static constexpr int TS = sizeof(T) == 4 ? (NB == 12 ? 4 : NB == 8 ? 4 : NB == 6 ? 2 : NB == 4 ? 2 : 1)
+                                             : (NB == 8 ? 4 : NB == 6 ? 2 : NB == 4 ? 2 : 1);
+    static constexpr int RPL = NB / TS;
+    static constexpr int THREADS = 128;
+    static constexpr int NT = THREADS / TS;
+    static constexpr bool OK = (sizeof(T) == 4 ? NB <= 12 : NB <= 8) && NB % TS == 0;
+    static __host__ __device__ size_t bytes(int N, int m, bool fact, bool solve) {
+        return ((fact ? (size_t)N * Dims<T, NB>::BLK : 0) + (solve ? (size_t)N * m * Dims<T, NB>::LD : 0)) *
+               sizeof(T);
+    }
+};
+
+// Cholesky of the team's block with every lane collecting the whole factor: on return Lf[j][k]
+// (j >= k) = L[j][k] and Linv[k] = 1/L[k][k] in every lane; a[][] holds the lane's rows of L.
+template <typename T, int NB, int TS, int RPL>
+__device__ __forceinline__ int team_potrf_full(T (&a)[RPL][NB], T (&Lf)[NB][NB], T (&Linv)[NB],
+                                               const Lane<NB, TS> &ln) {
+    int bad = -1;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const T akk = __shfl_sync(kFull, a[k / TS][k], ln.base + k % TS);
+        bad = (!(akk > T(0)) && bad < 0) ? k : bad;
+        const T d = sqrt_rn(akk);
+        const T inv = rcp_rn(d);
+        Lf[k][k] = d;
+        Linv[k] = inv;
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) a[t][k] = (ln.row(t) == k) ? d : a[t][k] * inv;
+#pragma unroll
+        for (int j = k + 1; j < NB; ++j) {
+            const T ljk = __shfl_sync(kFull, a[j / TS][k], ln.base + j % TS);
+            Lf[j][k] = ljk;
+#pragma unroll
+            for (int t = 0; t < RPL; ++t) a[t][j] = fma(-a[t][k], ljk, a[t][j]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < RPL; ++t)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) a[t][j] = (j > ln.row(t)) ? T(0) : a[t][j];
+    return bad;
+}
+
+// x <- L^{-1} x with L in registers (per-lane vectors).
+template <typename T, int NB, int RPL>
+__device__ __forceinline__ void tri_solve_reg(T (&x)[RPL][NB], const T (&Lf)[NB][NB], const T (&Linv)[NB]) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+            x[t][k] *= Linv[k];
+#pragma unroll
+            for (int j = k + 1; j < NB; ++j) x[t][j] = fma(-x[t][k], Lf[j][k], x[t][j]);
+        }
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void fwd_full(T (&y)[NB], const T (&Lf)[NB][NB], const T (&Linv)[NB]) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        y[k] *= Linv[k];
+#pragma unroll
+        for (int j = k + 1; j < NB; ++j) y[j] = fma(-y[k], Lf[j][k], y[j]);
+    }
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void bwd_full(T (&v)[NB], const T (&Lf)[NB][NB], const T (&Linv)[NB]) {
+#pragma unroll
+    for (int k = NB - 1; k >= 0; --k) {
+        v[k] *= Linv[k];
+#pragma unroll
+        for (int i = 0; i < k; ++i) v[i] = fma(-Lf[k][i], v[k], v[i]);
+    }
+}
+
+// Whole L^ diagonal block of original block c into registers (every lane), from global Dhat.
+template <typename T, int NB>
+__device__ __forceinline__ void load_L_full(T (&Lf)[NB][NB], T (&Linv)[NB], const T *blk, int n) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        T row[NB];
+        g_load_row1<T, NB>(row, blk, n, i, true, true);
+#pragma unroll
+        for (int k = 0; k <= i; ++k) Lf[i][k] = row[k];
+        Linv[i] = rcp_rn(row[i]);
+    }
+}
+
+template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE, int MR>
+__global__ void __launch_bounds__(NT *TS, 2)
+    btd_fused_r_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C,
+                       T *x, int32_t *info, Geo g, int sys0) {
+    constexpr int LD = Dims<T, NB>::LD, BLK = Dims<T, NB>::BLK;
+    constexpr int RPL = NB / TS;
+    constexpr int TPW = 32 / TS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *slots = reinterpret_cast<T *>(smem_raw);
+    __shared__ unsigned s_fail;
+
+    const int N = g.N, n = g.n;
+    const int m = MR > 0 ? MR : g.m;
+    T *Y = slots + (FACT ? (size_t)N * BLK : 0);
+    const long long sys = (long long)blockIdx.x + sys0;
+    const size_t nn = (size_t)n * n;
+    const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
+    T *Dh = Dhat + sys * N * nn;
+    T *Cs = C + sys * (size_t)g.nC * nn;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, team = tid / TS;
+    Lane<NB, TS> ln{lane % TS, lane - lane % TS};
+
+    if (tid == 0) s_fail = 0xffffffffu;
+    fused_load_inputs<T, NB, FACT, SOLVE>(slots, Y, D ? D + sys * N * nn : nullptr,
+                                          SOLVE ? bvec + sys * (size_t)N * n * m : nullptr, N, n, m);
     __syncthreads();
 
-    // ---- levels l = 1..L (stride s): a2-a6
     for (int l = 1; l <= g.L; ++l) {
         const int s = 1 << (l - 1);
         const int ncols = ((N / s) + 1) / 2;
         const long long offL = g.off[l - 1];
-        const long long offN = g.off[l];
         for (int j0 = 0; j0 < ncols; j0 += NT) {
             const int j = j0 + team;
-            const bool wact = j0 + warp * TPW < ncols;  // warp has at least one active team
+            const bool wact = j0 + warp * TPW < ncols;
             const bool act = j < ncols;
-            const int c = s * (2 * j + 1);
+            const int c = act ? s * (2 * j + 1) : s;  // inactive teams shadow a valid column, store nothing
             const bool hasL = act && c > s;
             const bool hasR = act && (c + s <= N);
-            T cl[NB];
+            T cl[RPL][NB];  // lane's columns of the left coupling (kept for phase Y)
+            T SL[RPL][NB];  // lane's rows of C_l^T C_l (left downdate, applied in phase Y)
             if (wact) {
-                // -- a3: D~_c -> D^_c
-                T dl[NB];
+                T Lf[NB][NB], Linv[NB];
+                T cr[RPL][NB];
                 if (FACT) {
-                    vload<T, NB>(dl, slots + (size_t)((act ? c : 1) - 1) * BLK + rr * LD);
-                    if (!(act && rv)) {
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) dl[q] = (q == r) ? T(1) : T(0);
-                    }
-                    const int bad = team_potrf<T, NB>(dl, r, base);
-                    if (act && bad >= 0 && r == 0) atomicMin(&s_fail, fail_key(c));
-                    g_store_row<T, NB>(Dh + (size_t)(c - 1) * nn, dl, n, r, act);
-                } else {
-                    g_load_row<T, NB>(dl, Dh + (size_t)(c - 1) * nn, n, r, act, true);
-                }
-                team_put_Lt<T, NB>(sLt, dl, r);
-
-                // -- a4: couplings. cr = row r of the right coupling, cl = column r of the left one.
-                T cr[NB];
-                if (FACT) {
+                    // -- a3: D~_c -> D^_c
+                    T a[RPL][NB];
+                    s_load_rows<T, NB, TS, RPL>(a, slots + (size_t)(c - 1) * BLK, ln);
+                    if (!act) set_identity<T, NB, TS, RPL>(a, ln);
+                    const int bad = team_potrf_full<T, NB, TS, RPL>(a, Lf, Linv, ln);
+                    if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
+                    g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
+                    // -- a4: couplings (row q+TS t of the right one, column q+TS t of the left one)
                     if (l == 1) {
-                        g_load_row<T, NB>(cr, Es + (size_t)(c - 1) * nn, n, r, hasR, false);  // E_c   = (c+1, c)
-                        g_load_col<T, NB>(cl, Es + (size_t)(c - 2) * nn, n, r, hasL, false);  // E_c-1 = (c, c-1)
+                        g_load_rows<T, NB, TS, RPL>(cr, Es + (size_t)(c - 1) * nn, n, ln, hasR, false);
+                        g_load_cols<T, NB, TS, RPL>(cl, Es + (size_t)((c >= 2 ? c : 2) - 2) * nn, n, ln, hasL, false);
                     } else {
-                        vload<T, NB>(cr, slots + (size_t)((hasR ? c + s / 2 : 1) - 1) * BLK + rr * LD);
-                        const T *pl = slots + (size_t)((hasL ? c - s / 2 : 1) - 1) * BLK + rr;
+                        s_load_rows<T, NB, TS, RPL>(cr, slots + (size_t)((hasR ? c + s / 2 : c) - 1) * BLK, ln);
+                        s_load_cols<T, NB, TS, RPL>(cl, slots + (size_t)((hasL ? c - s / 2 : c) - 1) * BLK, ln);
 #pragma unroll
-                        for (int q = 0; q < NB; ++q) cl[q] = pl[q * LD];
+                        for (int t = 0; t < RPL; ++t)
 #pragma unroll
-                        for (int q = 0; q < NB; ++q) {
-                            cr[q] = (hasR && rv) ? cr[q] : T(0);
-                            cl[q] = (hasL && rv) ? cl[q] : T(0);
-                        }
+                            for (int q = 0; q < NB; ++q) {
+                                cr[t][q] = hasR ? cr[t][q] : T(0);
+                                cl[t][q] = hasL ? cl[t][q] : T(0);
+                            }
                     }
-                    __syncwarp();
-                    tri_solve<T, NB>(cr, sLt);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
-                    tri_solve<T, NB>(cl, sLt);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
-                    g_store_row<T, NB>(Cs + (offL + c / s - 1) * nn, cr, n, r, hasR);
-                    g_store_col<T, NB>(Cs + (offL + c / s - 2) * nn, cl, n, r, hasL);
+                    tri_solve_reg<T, NB, RPL>(cr, Lf, Linv);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
+                    tri_solve_reg<T, NB, RPL>(cl, Lf, Linv);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
+                    g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
+                    g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
                 } else {
-                    g_load_row<T, NB>(cr, Cs + (offL + c / s - 1) * nn, n, r, hasR, false);
-                    g_load_col<T, NB>(cl, Cs + (offL + c / s - 2) * nn, n, r, hasL, false);
+                    load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
+                    g_load_rows<T, NB, TS, RPL>(cr, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
+                    g_load_cols<T, NB, TS, RPL>(cl, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
+                                                false);
                 }
-                T inv_r = T(1);
-                if (SOLVE) {
-                    __syncwarp();
-                    inv_r = sLt[rr * LD + rr];  // 1/L[r][r] (team_put_Lt)
-                }
-                __syncwarp();  // sLt is dead from here on; sCl reuses it
-                if (rv) {
-                    vstore<T, NB>(sCr + r * LD, cr);
-                    vstore<T, NB>(sClT + r * LD, cl);
-#pragma unroll
-                    for (int q = 0; q < NB; ++q) sCl[q * LD + r] = cl[q];
-                }
-                __syncwarp();
-
-                if (FACT) {
-                    // -- a5: fill  C_{l+1,(c-s)/2s} = -C_r C_l  -> slot[c] (column c's D~ is consumed)
-                    if (hasL && hasR && rv) {
-                        T f[NB];
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) f[q] = T(0);
-                        rowmat_sub<T, NB>(f, cr, sCl);
-                        vstore<T, NB>(slots + (size_t)(c - 1) * BLK + r * LD, f);
-                    }
-                    // -- a2 (right): D~_{c+s} -= C_r C_r^T
-                    if (hasR && rv) {
-                        T acc[NB];
-                        T *p = slots + (size_t)(c + s - 1) * BLK + r * LD;
-                        vload<T, NB>(acc, p);
-                        rowdot_sub<T, NB>(acc, cr, sCr);
-                        vstore<T, NB>(p, acc);
-                    }
-                }
-                (void)offN;
-                // -- a6: y_c <- D^^{-1} y_c ; y_{c+s} -= C_r y_c
+                // -- a6: y_c <- D^^{-1} y_c (redundantly in every lane of the team), y_{c+s} -= C_r y_c
                 if (SOLVE) {
                     for (int q = 0; q < m; ++q) {
-                        T *yc = Y + ((size_t)((act ? c : 1) - 1) * m + q) * LD;
-                        T yv = yc[rr];
-                        yv = (act && rv) ? yv : T(0);
-                        yv = team_fwd<T, NB>(yv, dl, inv_r, r, base);
-                        if (act && rv) yc[r] = yv;
-                    }
-                    __syncwarp();
-                    if (hasR && rv) {
-                        for (int q = 0; q < m; ++q) {
-                            const T d = dot<T, NB>(cr, Y + ((size_t)(c - 1) * m + q) * LD);
-                            Y[((size_t)(c + s - 1) * m + q) * LD + r] -= d;
+                        T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
+                        T yv[NB];
+                        vload<T, NB>(yv, yc);
+                        fwd_full<T, NB>(yv, Lf, Linv);
+                        __syncwarp();
+#pragma unroll
+                        for (int t = 0; t < RPL; ++t) {
+                            if (act) yc[ln.row(t)] = select_idx<T, NB>(yv, ln.row(t));
+                            if (hasR) {
+                                T d = T(0);
+#pragma unroll
+                                for (int k = 0; k < NB; ++k) d = fma(cr[t][k], yv[k], d);
+                                Y[((size_t)(c + s - 1) * m + q) * LD + ln.row(t)] -= d;
+                            }
                         }
+                    }
+                }
+                if (FACT) {
+                    // -- a2 (right): D~_{c+s} -= C_r C_r^T   (rows of C_r exchanged by shuffles)
+                    {
+                        T SR[RPL][NB];
+                        set_zero<T, NB, RPL>(SR);
+#pragma unroll
+                        for (int jj = 0; jj < NB; ++jj)
+#pragma unroll
+                            for (int k = 0; k < NB; ++k) {
+                                const T v = __shfl_sync(kFull, cr[jj / TS][k], ln.base + jj % TS);  // C_r[jj][k]
+#pragma unroll
+                                for (int t = 0; t < RPL; ++t) SR[t][jj] = fma(cr[t][k], v, SR[t][jj]);
+                            }
+                        if (hasR) {
+                            T *p = slots + (size_t)(c + s - 1) * BLK;
+#pragma unroll
+                            for (int t = 0; t < RPL; ++t) {
+                                T acc[NB];
+                                vload<T, NB>(acc, p + ln.row(t) * LD);
+#pragma unroll
+                                for (int q = 0; q < NB; ++q) acc[q] -= SR[t][q];
+                                vstore<T, NB>(p + ln.row(t) * LD, acc);
+                            }
+                        }
+                    }
+                    // -- a5 fill -C_r C_l -> slot[c], and C_l^T C_l for phase Y (columns of C_l shuffled)
+                    {
+                        T F[RPL][NB];
+                        set_zero<T, NB, RPL>(F);
+                        set_zero<T, NB, RPL>(SL);
+#pragma unroll
+                        for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+                            for (int k = 0; k < NB; ++k) {
+                                const T v = __shfl_sync(kFull, cl[bb / TS][k], ln.base + bb % TS);  // C_l[k][bb]
+#pragma unroll
+                                for (int t = 0; t < RPL; ++t) {
+                                    F[t][bb] = fma(-cr[t][k], v, F[t][bb]);
+                                    SL[t][bb] = fma(cl[t][k], v, SL[t][bb]);
+                                }
+                            }
+                        if (hasL && hasR) s_store_rows<T, NB, TS, RPL>(slots + (size_t)(c - 1) * BLK, F, ln);
                     }
                 }
             }
             __syncthreads();
             // ---- phase Y: left pushes (deferred left-looking part of Alg. 4, l.7/l.9)
-            if (wact && hasL && rv) {
+            if (wact && hasL) {
                 if (FACT) {
-                    T acc[NB];
-                    T *p = slots + (size_t)(c - s - 1) * BLK + r * LD;
-                    vload<T, NB>(acc, p);
-                    rowdot_sub<T, NB>(acc, cl, sClT);  // D~_{c-s} -= C_l^T C_l
-                    vstore<T, NB>(p, acc);
+                    T *p = slots + (size_t)(c - s - 1) * BLK;
+#pragma unroll
+                    for (int t = 0; t < RPL; ++t) {
+                        T acc[NB];
+                        vload<T, NB>(acc, p + ln.row(t) * LD);
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) acc[q] -= SL[t][q];  // D~_{c-s} -= C_l^T C_l
+                        vstore<T, NB>(p + ln.row(t) * LD, acc);
+                    }
                 }
                 if (SOLVE) {
                     for (int q = 0; q < m; ++q) {
-                        const T d = dot<T, NB>(cl, Y + ((size_t)(c - 1) * m + q) * LD);
-                        Y[((size_t)(c - s - 1) * m + q) * LD + r] -= d;  // y_{c-s} -= C_l^T y_c
+                        const T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
+#pragma unroll
+                        for (int t = 0; t < RPL; ++t)  // y_{c-s} -= C_l^T y_c
+                            Y[((size_t)(c - s - 1) * m + q) * LD + ln.row(t)] -= dot<T, NB>(cl[t], yc);
                     }
                 }
             }
@@ -275,39 +377,270 @@ __global__ void __launch_bounds__(NT *TS, FusedCfg<T, NB>::MINB)
                 if (j0 + warp * TPW >= ncols) continue;  // warp-uniform
                 const int j = j0 + team;
                 const bool act = j < ncols;
-                const int c = s * (2 * j + 1);
+                const int c = act ? s * (2 * j + 1) : s;
                 const bool hasL = act && c > s;
                 const bool hasR = act && (c + s <= N);
-                T lc[NB], crc[NB], clr[NB];
-                g_load_col<T, NB>(lc, Dh + (size_t)(c - 1) * nn, n, r, act, true);
-                g_load_col<T, NB>(crc, Cs + (offL + c / s - 1) * nn, n, r, hasR, false);
-                g_load_row<T, NB>(clr, Cs + (offL + c / s - 2) * nn, n, r, hasL, false);
-                const T dg = Dh[(size_t)((act ? c : 1) - 1) * nn + (size_t)(r < n ? r : 0) * (n + 1)];
-                const T inv_r = (act && r < n) ? T(1) / dg : T(1);
+                T Lf[NB][NB], Linv[NB];
+                load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
+                T crc[RPL][NB], clr[RPL][NB];
+                g_load_cols<T, NB, TS, RPL>(crc, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
+                g_load_rows<T, NB, TS, RPL>(clr, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
+                                            false);
                 for (int q = 0; q < m; ++q) {
-                    T *yc = Y + ((size_t)((act ? c : 1) - 1) * m + q) * LD;
-                    T v = yc[rr];
-                    v = (act && rv) ? v : T(0);
-                    const T a = dot<T, NB>(crc, Y + ((size_t)((hasR ? c + s : 1) - 1) * m + q) * LD);
-                    const T b2 = dot<T, NB>(clr, Y + ((size_t)((hasL ? c - s : 1) - 1) * m + q) * LD);
-                    v -= hasR ? a : T(0);
-                    v -= hasL ? b2 : T(0);
-                    v = team_bwd<T, NB>(v, lc, inv_r, r, base);
-                    if (act && rv) yc[r] = v;
+                    T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
+                    const T *xr = Y + ((size_t)((hasR ? c + s : c) - 1) * m + q) * LD;
+                    const T *xl = Y + ((size_t)((hasL ? c - s : c) - 1) * m + q) * LD;
+                    T v[NB];
+                    vload<T, NB>(v, yc);
+                    T mine[RPL];
+#pragma unroll
+                    for (int t = 0; t < RPL; ++t) {
+                        const T a = dot<T, NB>(crc[t], xr);  // (C_r^T x_{c+s})[i]
+                        const T b2 = dot<T, NB>(clr[t], xl);  // (C_l x_{c-s})[i]
+                        mine[t] = select_idx<T, NB>(v, ln.row(t));
+                        mine[t] -= hasR ? a : T(0);
+                        mine[t] -= hasL ? b2 : T(0);
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int t = 0; t < RPL; ++t)
+                        if (act) yc[ln.row(t)] = mine[t];
+                    __syncwarp();
+                    vload<T, NB>(v, yc);
+                    bwd_full<T, NB>(v, Lf, Linv);
+                    __syncwarp();
+#pragma unroll
+                    for (int t = 0; t < RPL; ++t)
+                        if (act) yc[ln.row(t)] = select_idx<T, NB>(v, ln.row(t));
                 }
             }
             __syncthreads();
         }
-        T *xs = x + sys * (size_t)N * n * m;
-        for (size_t q = tid; q < (size_t)N * n * m; q += blockDim.x) {
-            const int i = (int)(q / ((size_t)n * m)), rem = (int)(q % ((size_t)n * m));
-            const int r2 = rem / m, qq = rem % m;
-            xs[q] = Y[((size_t)i * m + qq) * LD + r2];
-        }
+        fused_store_x<T, NB>(x + sys * (size_t)N * n * m, Y, N, n, m);
     }
     if (FACT && tid == 0) info[sys] = (s_fail == 0xffffffffu) ? 0 : (int)(s_fail & ((1u << 25) - 1));
 }
 
+// ============================================================================ FUSED-S
+//
+// Shared memory (elements of T):
+//   slots   N * BLK            (FACT only)
+//   Y       N * m * LD         (SOLVE only; y then x, one padded row per block and rhs)
+//   scratch NT * TSTR          (3 blocks per team: sLt (later reused as sCl), sCr, sClT;
+//                               TSTR padded by 64 B so the two teams of a warp hit different banks)
+template <typename T, int NB, int NT>
+struct FusedSmem {
+    static constexpr int LD = Dims<T, NB>::LD;
+    static constexpr int BLK = Dims<T, NB>::BLK;
+    static constexpr int TSTR = 3 * BLK + 64 / (int)sizeof(T);
+    static __host__ __device__ size_t bytes(int N, int m, bool fact, bool solve) {
+        size_t e = (fact ? (size_t)N * BLK : 0) + (solve ? (size_t)N * m * LD : 0) + (size_t)NT * TSTR;
+        return e * sizeof(T);
+    }
+};
+
+// Launch shape of the FUSED-S kernel for block size NB: team width TS, CTA threads, min CTAs/SM.
+template <typename T, int NB>
+struct FusedCfg {
+    static constexpr int TS = NB <= 1 ? 1 : NB <= 2 ? 2 : NB <= 4 ? 4 : NB <= 8 ? 8 : NB <= 16 ? 16 : 32;
+    static constexpr int LIM = sizeof(T) == 4 ? 16 : 8;  // register rows per lane that fit 128 regs
+    static constexpr int THREADS = NB <= LIM ? 256 : 128;
+    static constexpr int NT = THREADS / TS;
+    static constexpr int MINB = NB <= LIM ? 2 : 1;
+};
+
+// MR = number of right-hand sides if fixed at compile time (1), 0 = runtime g.m.
+template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE, int MR>
+__global__ void __launch_bounds__(NT *TS, FusedCfg<T, NB>::MINB)
+    btd_fused_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C,
+                     T *x, int32_t *info, Geo g, int sys0) {
+    using S = FusedSmem<T, NB, NT>;
+    constexpr int LD = S::LD, BLK = S::BLK;
+    constexpr int TPW = 32 / TS;  // teams per warp
+    constexpr int RPL = 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *smem = reinterpret_cast<T *>(smem_raw);
+    T *slots = smem;
+    T *Y = smem + (FACT ? (size_t)g.N * BLK : 0);
+    __shared__ unsigned s_fail;
+
+    const int N = g.N, n = g.n;
+    const int m = MR > 0 ? MR : g.m;
+    T *scr = Y + (SOLVE ? (size_t)N * m * LD : 0);
+    const long long sys = (long long)blockIdx.x + sys0;
+    const size_t nn = (size_t)n * n;
+    const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
+    T *Dh = Dhat + sys * N * nn;
+    T *Cs = C + sys * (size_t)g.nC * nn;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, team = tid / TS;
+    Lane<NB, TS> ln{lane % TS, lane - lane % TS};
+    const bool rv = ln.valid(0);
+    T *sLt = scr + (size_t)team * S::TSTR;
+    T *sCl = sLt;  // reuses sLt once both TRSMs are done
+    T *sCr = sLt + BLK;
+    T *sClT = sCr + BLK;
+
+    if (tid == 0) s_fail = 0xffffffffu;
+    fused_load_inputs<T, NB, FACT, SOLVE>(slots, Y, D ? D + sys * N * nn : nullptr,
+                                          SOLVE ? bvec + sys * (size_t)N * n * m : nullptr, N, n, m);
+    __syncthreads();
+
+    for (int l = 1; l <= g.L; ++l) {
+        const int s = 1 << (l - 1);
+        const int ncols = ((N / s) + 1) / 2;
+        const long long offL = g.off[l - 1];
+        for (int j0 = 0; j0 < ncols; j0 += NT) {
+            const int j = j0 + team;
+            const bool wact = j0 + warp * TPW < ncols;
+            const bool act = j < ncols;
+            const int c = act ? s * (2 * j + 1) : s;
+            const bool hasL = act && c > s;
+            const bool hasR = act && (c + s <= N);
+            T cl[RPL][NB];
+            if (wact) {
+                T dl[RPL][NB], dinv[RPL];
+                if (FACT) {
+                    s_load_rows<T, NB, TS, RPL>(dl, slots + (size_t)(c - 1) * BLK, ln);
+                    if (!act) set_identity<T, NB, TS, RPL>(dl, ln);
+                    const int bad = team_potrf<T, NB, TS, RPL>(dl, dinv, ln);
+                    if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
+                    g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, dl, n, ln, act);
+                } else {
+                    g_load_rows<T, NB, TS, RPL>(dl, Dh + (size_t)(c - 1) * nn, n, ln, act, true);
+                    dinv[0] = T(1);
+#pragma unroll
+                    for (int k = 0; k < NB; ++k) dinv[0] = (k == ln.q) ? rcp_rn(dl[0][k]) : dinv[0];
+                }
+                team_put_Lt<T, NB, TS, RPL>(sLt, dl, dinv, ln);
+
+                T cr[RPL][NB];
+                if (FACT) {
+                    if (l == 1) {
+                        g_load_rows<T, NB, TS, RPL>(cr, Es + (size_t)(c - 1) * nn, n, ln, hasR, false);
+                        g_load_cols<T, NB, TS, RPL>(cl, Es + (size_t)((c >= 2 ? c : 2) - 2) * nn, n, ln, hasL, false);
+                    } else {
+                        s_load_rows<T, NB, TS, RPL>(cr, slots + (size_t)((hasR ? c + s / 2 : c) - 1) * BLK, ln);
+                        s_load_cols<T, NB, TS, RPL>(cl, slots + (size_t)((hasL ? c - s / 2 : c) - 1) * BLK, ln);
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) {
+                            cr[0][q] = (hasR && rv) ? cr[0][q] : T(0);
+                            cl[0][q] = (hasL && rv) ? cl[0][q] : T(0);
+                        }
+                    }
+                    __syncwarp();
+                    tri_solve<T, NB, RPL>(cr, sLt);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
+                    tri_solve<T, NB, RPL>(cl, sLt);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
+                    g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
+                    g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
+                } else {
+                    g_load_rows<T, NB, TS, RPL>(cr, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
+                    g_load_cols<T, NB, TS, RPL>(cl, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
+                                                false);
+                }
+                __syncwarp();  // sLt is dead from here on; sCl reuses it
+                s_store_rows<T, NB, TS, RPL>(sCr, cr, ln);
+                s_store_rows<T, NB, TS, RPL>(sClT, cl, ln);
+                s_store_cols<T, NB, TS, RPL>(sCl, cl, ln);
+                __syncwarp();
+
+                if (FACT) {
+                    // -- a5: fill  C_{l+1,(c-s)/2s} = -C_r C_l  -> slot[c] (column c's D~ is consumed)
+                    if (hasL && hasR) {
+                        T f[RPL][NB];
+                        set_zero<T, NB, RPL>(f);
+                        rowmat_sub<T, NB, RPL>(f, cr, sCl);
+                        s_store_rows<T, NB, TS, RPL>(slots + (size_t)(c - 1) * BLK, f, ln);
+                    }
+                    // -- a2 (right): D~_{c+s} -= C_r C_r^T
+                    if (hasR) {
+                        T acc[RPL][NB];
+                        T *p = slots + (size_t)(c + s - 1) * BLK;
+                        s_load_rows<T, NB, TS, RPL>(acc, p, ln);
+                        rowdot_sub<T, NB, RPL>(acc, cr, sCr);
+                        s_store_rows<T, NB, TS, RPL>(p, acc, ln);
+                    }
+                }
+                // -- a6: y_c <- D^^{-1} y_c ; y_{c+s} -= C_r y_c
+                if (SOLVE) {
+                    for (int q = 0; q < m; ++q) {
+                        T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
+                        T yv[RPL];
+                        yv[0] = yc[rv ? ln.q : 0];
+                        yv[0] = (act && rv) ? yv[0] : T(0);
+                        team_fwd<T, NB, TS, RPL>(yv, dl, dinv, ln);
+                        if (act && rv) yc[ln.q] = yv[0];
+                    }
+                    __syncwarp();
+                    if (hasR && rv) {
+                        for (int q = 0; q < m; ++q) {
+                            const T d = dot<T, NB>(cr[0], Y + ((size_t)(c - 1) * m + q) * LD);
+                            Y[((size_t)(c + s - 1) * m + q) * LD + ln.q] -= d;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- phase Y: left pushes (deferred left-looking part of Alg. 4, l.7/l.9)
+            if (wact && hasL) {
+                if (FACT) {
+                    T acc[RPL][NB];
+                    T *p = slots + (size_t)(c - s - 1) * BLK;
+                    s_load_rows<T, NB, TS, RPL>(acc, p, ln);
+                    rowdot_sub<T, NB, RPL>(acc, cl, sClT);  // D~_{c-s} -= C_l^T C_l
+                    s_store_rows<T, NB, TS, RPL>(p, acc, ln);
+                }
+                if (SOLVE && rv) {
+                    for (int q = 0; q < m; ++q) {
+                        const T d = dot<T, NB>(cl[0], Y + ((size_t)(c - 1) * m + q) * LD);
+                        Y[((size_t)(c - s - 1) * m + q) * LD + ln.q] -= d;  // y_{c-s} -= C_l^T y_c
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    // ---- a7: backward sweep, l = L..1 (Alg. 6 lines 10-16)
+    if (SOLVE) {
+        for (int l = g.L; l >= 1; --l) {
+            const int s = 1 << (l - 1);
+            const int ncols = ((N / s) + 1) / 2;
+            const long long offL = g.off[l - 1];
+            for (int j0 = 0; j0 < ncols; j0 += NT) {
+                if (j0 + warp * TPW >= ncols) continue;  // warp-uniform
+                const int j = j0 + team;
+                const bool act = j < ncols;
+                const int c = act ? s * (2 * j + 1) : s;
+                const bool hasL = act && c > s;
+                const bool hasR = act && (c + s <= N);
+                T lc[RPL][NB], crc[RPL][NB], clr[RPL][NB], dinv[RPL];
+                g_load_cols<T, NB, TS, RPL>(lc, Dh + (size_t)(c - 1) * nn, n, ln, act, true);
+                g_load_cols<T, NB, TS, RPL>(crc, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
+                g_load_rows<T, NB, TS, RPL>(clr, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
+                                            false);
+                dinv[0] = T(1);
+#pragma unroll
+                for (int k = 0; k < NB; ++k) dinv[0] = (k == ln.q) ? rcp_rn(lc[0][k]) : dinv[0];
+                for (int q = 0; q < m; ++q) {
+                    T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
+                    T v[RPL];
+                    v[0] = yc[rv ? ln.q : 0];
+                    v[0] = (act && rv) ? v[0] : T(0);
+                    const T a = dot<T, NB>(crc[0], Y + ((size_t)((hasR ? c + s : c) - 1) * m + q) * LD);
+                    const T b2 = dot<T, NB>(clr[0], Y + ((size_t)((hasL ? c - s : c) - 1) * m + q) * LD);
+                    v[0] -= hasR ? a : T(0);
+                    v[0] -= hasL ? b2 : T(0);
+                    team_bwd<T, NB, TS, RPL>(v, lc, dinv, ln);
+                    if (act && rv) yc[ln.q] = v[0];
+                }
+            }
+            __syncthreads();
+        }
+        fused_store_x<T, NB>(x + sys * (size_t)N * n * m, Y, N, n, m);
+    }
+    if (FACT && tid == 0) info[sys] = (s_fail == 0xffffffffu) ? 0 : (int)(s_fail & ((1u << 25) - 1));
+}
 
 // ============================================================================ LEVEL
 //
@@ -326,7 +659,7 @@ __global__ void btd_level_init_kernel(const T *__restrict__ D, const T *__restri
 }
 
 // One level l of Alg. 4 (FACT) and/or the forward sweep of Alg. 6 (SOLVE), deferred form.
-// grid = (ceil(ncols / NT), batch); one team per column; dynamic smem NT * LevelSmem::TSTR.
+// grid = (ceil(ncols / NT), batch); one team (one row per lane) per column; dynamic smem NT * TSTR.
 template <typename T, int NB>
 struct LevelSmem {
     static constexpr int BLK = Dims<T, NB>::BLK;
@@ -337,6 +670,7 @@ template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE>
 __global__ void __launch_bounds__(NT *TS) btd_level_fwd_kernel(const T *__restrict__ E, T *Dhat, T *C, T *x,
                                                               int32_t *info, Geo g, int l, int sys0) {
     constexpr int LD = Dims<T, NB>::LD, BLK = Dims<T, NB>::BLK;
+    constexpr int RPL = 1;
     extern __shared__ __align__(16) unsigned char lsm_raw[];
     T *scr_all = reinterpret_cast<T *>(lsm_raw);
 
@@ -348,8 +682,10 @@ __global__ void __launch_bounds__(NT *TS) btd_level_fwd_kernel(const T *__restri
     T *Cs = C + sys * (size_t)g.nC * nn;
     T *xs = x ? x + sys * (size_t)N * n * m : nullptr;
 
-    const int tid = threadIdx.x, lane = tid & 31, team = tid / TS, r = lane % TS, base = lane - r;
-    const bool rv = r < NB;
+    const int tid = threadIdx.x, lane = tid & 31, team = tid / TS;
+    Lane<NB, TS> ln{lane % TS, lane - lane % TS};
+    const int r = ln.q;
+    const bool rv = ln.valid(0);
     T *sLt = scr_all + team * LevelSmem<T, NB>::TSTR;
     T *sB = sLt + BLK;  // right coupling rows / deferred coupling rows / y broadcast
     T *sCl = sB + BLK;  // left coupling, row-major
@@ -358,7 +694,7 @@ __global__ void __launch_bounds__(NT *TS) btd_level_fwd_kernel(const T *__restri
     const int ncols = ((N / s) + 1) / 2;
     const int j = blockIdx.x * NT + team;
     const bool act = j < ncols;
-    const int c = s * (2 * j + 1);
+    const int c = act ? s * (2 * j + 1) : s;
     const bool hasL = act && c > s;
     const bool hasR = act && (c + s <= N);
     const bool defC = act && l > 1 && (c + s / 2 <= N);      // Alg. 4 l.7
@@ -367,126 +703,122 @@ __global__ void __launch_bounds__(NT *TS) btd_level_fwd_kernel(const T *__restri
     // Deferred left downdate (Alg. 4 l.7 / l.9):  acc -= Cd^T Cd  where Cd is the stored left
     // coupling of column ysrc at level l-1 (lane r: acc[j] -= sum_k Cd[k][r] Cd[k][j]), and its
     // forward-sweep analogue  y_tgt -= Cd^T y_ysrc.
-    auto deferred = [&](T(&acc)[NB], bool on, long long slot, int ysrc, int ytgt) {
-        T cdc[NB];
-        g_load_col<T, NB>(cdc, Cs + slot * nn, n, r, on, false);
+    auto deferred = [&](T(&acc)[RPL][NB], bool on, long long slot, int ysrc, int ytgt) {
+        T cdc[RPL][NB];
+        g_load_cols<T, NB, TS, RPL>(cdc, Cs + slot * nn, n, ln, on, false);
         if (FACT) {
             __syncwarp();
-            if (rv) {
-                T row[NB];
-                g_load_row<T, NB>(row, Cs + slot * nn, n, r, on, false);
-                vstore<T, NB>(sB + r * LD, row);
-            }
+            T row[RPL][NB];
+            g_load_rows<T, NB, TS, RPL>(row, Cs + slot * nn, n, ln, on, false);
+            s_store_rows<T, NB, TS, RPL>(sB, row, ln);
             __syncwarp();
-            if (on) rowmat_sub<T, NB>(acc, cdc, sB);
+            if (on) rowmat_sub<T, NB, RPL>(acc, cdc, sB);
         }
         if (SOLVE && on && r < n) {
             for (int q = 0; q < m; ++q) {
                 T sum = T(0);
 #pragma unroll
                 for (int k = 0; k < NB; ++k)
-                    if (k < n) sum = fma(cdc[k], xs[((size_t)(ysrc - 1) * n + k) * m + q], sum);
+                    if (k < n) sum = fma(cdc[0][k], xs[((size_t)(ysrc - 1) * n + k) * m + q], sum);
                 xs[((size_t)(ytgt - 1) * n + r) * m + q] -= sum;
             }
         }
     };
 
     // ---- D^_c: l.7 then l.8
+    T dinv[RPL];
     {
-        T dl[NB];
-        g_load_row<T, NB>(dl, Dh + (size_t)(c - 1) * nn, n, r, act, true);
+        T dl[RPL][NB];
+        g_load_rows<T, NB, TS, RPL>(dl, Dh + (size_t)(c - 1) * nn, n, ln, act, true);
         if (l > 1) deferred(dl, defC, cslot(g, l - 1, 2 * c / s), c + s / 2, c);
         if (FACT) {
-            const int bad = team_potrf<T, NB>(dl, r, base);
+            const int bad = team_potrf<T, NB, TS, RPL>(dl, dinv, ln);
             if (act && bad >= 0 && r == 0) report_fail(info + sys, c);
-            g_store_row<T, NB>(Dh + (size_t)(c - 1) * nn, dl, n, r, act);
+            g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, dl, n, ln, act);
         } else {
 #pragma unroll
-            for (int q = 0; q < NB; ++q)
-                if (q > r) dl[q] = T(0);
+            for (int q = 0; q < NB; ++q) dl[0][q] = (q > r) ? T(0) : dl[0][q];
+            dinv[0] = T(1);
+#pragma unroll
+            for (int k = 0; k < NB; ++k) dinv[0] = (k == r) ? rcp_rn(dl[0][k]) : dinv[0];
         }
         __syncwarp();
-        team_put_Lt<T, NB>(sLt, dl, r);
+        team_put_Lt<T, NB, TS, RPL>(sLt, dl, dinv, ln);
     }
     // ---- separator D^_{c+s}: l.9 (deferred, level l-1) then l.11 (this level)
-    T cr[NB];
+    T cr[RPL][NB];
     if (FACT) {
         if (l == 1)
-            g_load_row<T, NB>(cr, Es + (size_t)(c - 1) * nn, n, r, hasR, false);  // E_c = block (c+1, c)
+            g_load_rows<T, NB, TS, RPL>(cr, Es + (size_t)(c - 1) * nn, n, ln, hasR, false);  // E_c = (c+1, c)
         else
-            g_load_row<T, NB>(cr, Cs + cslot(g, l, c / s) * nn, n, r, hasR, false);
+            g_load_rows<T, NB, TS, RPL>(cr, Cs + cslot(g, l, c / s) * nn, n, ln, hasR, false);
         __syncwarp();
-        tri_solve<T, NB>(cr, sLt);  // l.10
-        g_store_row<T, NB>(Cs + cslot(g, l, c / s) * nn, cr, n, r, hasR);
-        T sep[NB];
-        g_load_row<T, NB>(sep, Dh + (size_t)(c + s - 1) * nn, n, r, hasR, false);
+        tri_solve<T, NB, RPL>(cr, sLt);  // l.10
+        g_store_rows<T, NB, TS, RPL>(Cs + cslot(g, l, c / s) * nn, cr, n, ln, hasR);
+        T sep[RPL][NB];
+        g_load_rows<T, NB, TS, RPL>(sep, Dh + (size_t)((hasR ? c + s : c) - 1) * nn, n, ln, hasR, false);
         if (l > 1) deferred(sep, defS, cslot(g, l - 1, 2 * c / s + 2), c + s + s / 2, c + s);
         __syncwarp();
-        if (rv) vstore<T, NB>(sB + r * LD, cr);
+        s_store_rows<T, NB, TS, RPL>(sB, cr, ln);
         __syncwarp();
         if (hasR) {
-            rowdot_sub<T, NB>(sep, cr, sB);  // l.11: D^_{c+s} -= C_r C_r^T
-            g_store_row<T, NB>(Dh + (size_t)(c + s - 1) * nn, sep, n, r, hasR);
+            rowdot_sub<T, NB, RPL>(sep, cr, sB);  // l.11: D^_{c+s} -= C_r C_r^T
+            g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c + s - 1) * nn, sep, n, ln, hasR);
         }
         {
-            T cl[NB];
+            T cl[RPL][NB];
             if (l == 1)
-                g_load_col<T, NB>(cl, Es + (size_t)(c - 2) * nn, n, r, hasL, false);  // E_{c-1} = (c, c-1)
+                g_load_cols<T, NB, TS, RPL>(cl, Es + (size_t)((c >= 2 ? c : 2) - 2) * nn, n, ln, hasL, false);
             else
-                g_load_col<T, NB>(cl, Cs + cslot(g, l, c / s - 1) * nn, n, r, hasL, false);
-            tri_solve<T, NB>(cl, sLt);  // l.12
-            g_store_col<T, NB>(Cs + cslot(g, l, c / s - 1) * nn, cl, n, r, hasL);
-            if (rv) {
-#pragma unroll
-                for (int q = 0; q < NB; ++q) sCl[q * LD + r] = cl[q];
-            }
+                g_load_cols<T, NB, TS, RPL>(cl, Cs + cslot(g, l, (c / s >= 2 ? c / s : 2) - 1) * nn, n, ln, hasL,
+                                            false);
+            tri_solve<T, NB, RPL>(cl, sLt);  // l.12
+            g_store_cols<T, NB, TS, RPL>(Cs + cslot(g, l, c / s - 1) * nn, cl, n, ln, hasL);
+            s_store_cols<T, NB, TS, RPL>(sCl, cl, ln);
         }
         __syncwarp();
         if (hasL && hasR) {  // l.13: fill -> its final slot (trsm'd in place at level l+1)
-            T f[NB];
-#pragma unroll
-            for (int q = 0; q < NB; ++q) f[q] = T(0);
-            rowmat_sub<T, NB>(f, cr, sCl);
-            g_store_row<T, NB>(Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn, f, n, r, true);
+            T f[RPL][NB];
+            set_zero<T, NB, RPL>(f);
+            rowmat_sub<T, NB, RPL>(f, cr, sCl);
+            g_store_rows<T, NB, TS, RPL>(Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn, f, n, ln, true);
         }
     } else {
-        g_load_row<T, NB>(cr, Cs + cslot(g, l, c / s) * nn, n, r, hasR, false);
+        g_load_rows<T, NB, TS, RPL>(cr, Cs + cslot(g, l, c / s) * nn, n, ln, hasR, false);
         if (l > 1) {
-            T dummy[NB];
+            T dummy[RPL][NB];
+            set_zero<T, NB, RPL>(dummy);
             deferred(dummy, defS, cslot(g, l - 1, 2 * c / s + 2), c + s + s / 2, c + s);
         }
     }
     if (SOLVE) {
         // Alg. 6 l.4-5: y_c <- D^_c^{-1} y_c ; y_{c+s} -= C_r y_c   (l.6 is deferred like l.7/l.9)
-        T dl[NB];
+        T dl[RPL][NB];
 #pragma unroll
-        for (int k = 0; k < NB; ++k) dl[k] = (rv && k < r) ? sLt[k * LD + r] : T(0);
-        T inv_r = T(1);
-#pragma unroll
-        for (int k = 0; k < NB; ++k)
-            if (k == r) inv_r = sLt[k * LD + k];
+        for (int k = 0; k < NB; ++k) dl[0][k] = (rv && k < r) ? sLt[k * LD + (rv ? r : 0)] : T(0);
         for (int q = 0; q < m; ++q) {
-            T yv = (act && r < n) ? xs[((size_t)(c - 1) * n + r) * m + q] : T(0);
-            yv = team_fwd<T, NB>(yv, dl, inv_r, r, base);
-            if (act && r < n) xs[((size_t)(c - 1) * n + r) * m + q] = yv;
+            T yv[RPL];
+            yv[0] = (act && r < n) ? xs[((size_t)(c - 1) * n + r) * m + q] : T(0);
+            team_fwd<T, NB, TS, RPL>(yv, dl, dinv, ln);
+            if (act && r < n) xs[((size_t)(c - 1) * n + r) * m + q] = yv[0];
             __syncwarp();
-            if (rv) sB[r] = yv;
+            if (rv) sB[r] = yv[0];
             __syncwarp();
             if (hasR && r < n) {
                 T sum = T(0);
 #pragma unroll
-                for (int k = 0; k < NB; ++k) sum = fma(cr[k], sB[k], sum);
+                for (int k = 0; k < NB; ++k) sum = fma(cr[0][k], sB[k], sum);
                 xs[((size_t)(c + s - 1) * n + r) * m + q] -= sum;
             }
         }
     }
 }
 
-
 // Backward sweep level l (Alg. 6 lines 10-16): x_c = D^_c^{-T}(y_c - C_r^T x_{c+s} - C_l x_{c-s}).
 template <typename T, int NB, int TS, int NT>
 __global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, const T *C, T *x, Geo g, int l,
                                                               int sys0) {
+    constexpr int RPL = 1;
     __shared__ __align__(16) T sx[NT][2][NB];
     const int N = g.N, n = g.n, m = g.m;
     const long long sys = (long long)blockIdx.y + sys0;
@@ -494,37 +826,42 @@ __global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, co
     const T *Dh = Dhat + sys * N * nn;
     const T *Cs = C + sys * (size_t)g.nC * nn;
     T *xs = x + sys * (size_t)N * n * m;
-    const int tid = threadIdx.x, lane = tid & 31, team = tid / TS, r = lane % TS, base = lane - r;
-    const bool rv = r < NB;
+    const int tid = threadIdx.x, lane = tid & 31, team = tid / TS;
+    Lane<NB, TS> ln{lane % TS, lane - lane % TS};
+    const int r = ln.q;
+    const bool rv = ln.valid(0);
     const int s = 1 << (l - 1);
     const int ncols = ((N / s) + 1) / 2;
     const int j = blockIdx.x * NT + team;
     const bool act = j < ncols;
-    const int c = s * (2 * j + 1);
+    const int c = act ? s * (2 * j + 1) : s;
     const bool hasL = act && c > s;
     const bool hasR = act && (c + s <= N);
-    T lc[NB], crc[NB], clr[NB];
-    g_load_col<T, NB>(lc, Dh + (size_t)(c - 1) * nn, n, r, act, true);
-    g_load_col<T, NB>(crc, Cs + cslot(g, l, c / s) * nn, n, r, hasR, false);
-    g_load_row<T, NB>(clr, Cs + cslot(g, l, c / s - 1) * nn, n, r, hasL, false);
-    const T inv_r = (act && r < n) ? T(1) / Dh[(size_t)(c - 1) * nn + (size_t)r * n + r] : T(1);
+    T lc[RPL][NB], crc[RPL][NB], clr[RPL][NB], dinv[RPL];
+    g_load_cols<T, NB, TS, RPL>(lc, Dh + (size_t)(c - 1) * nn, n, ln, act, true);
+    g_load_cols<T, NB, TS, RPL>(crc, Cs + cslot(g, l, c / s) * nn, n, ln, hasR, false);
+    g_load_rows<T, NB, TS, RPL>(clr, Cs + cslot(g, l, (c / s >= 2 ? c / s : 2) - 1) * nn, n, ln, hasL, false);
+    dinv[0] = T(1);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) dinv[0] = (k == r) ? rcp_rn(lc[0][k]) : dinv[0];
     for (int q = 0; q < m; ++q) {
         if (rv) {
             sx[team][0][r] = (hasR && r < n) ? xs[((size_t)(c + s - 1) * n + r) * m + q] : T(0);
             sx[team][1][r] = (hasL && r < n) ? xs[((size_t)(c - s - 1) * n + r) * m + q] : T(0);
         }
         __syncwarp();
-        T v = (act && r < n) ? xs[((size_t)(c - 1) * n + r) * m + q] : T(0);
+        T v[RPL];
+        v[0] = (act && r < n) ? xs[((size_t)(c - 1) * n + r) * m + q] : T(0);
         T a = T(0), b2 = T(0);
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            a = fma(crc[k], sx[team][0][k], a);
-            b2 = fma(clr[k], sx[team][1][k], b2);
+            a = fma(crc[0][k], sx[team][0][k], a);
+            b2 = fma(clr[0][k], sx[team][1][k], b2);
         }
-        v -= a;
-        v -= b2;
-        v = team_bwd<T, NB>(v, lc, inv_r, r, base);
-        if (act && r < n) xs[((size_t)(c - 1) * n + r) * m + q] = v;
+        v[0] -= a;
+        v[0] -= b2;
+        team_bwd<T, NB, TS, RPL>(v, lc, dinv, ln);
+        if (act && r < n) xs[((size_t)(c - 1) * n + r) * m + q] = v[0];
         __syncwarp();
     }
 }
