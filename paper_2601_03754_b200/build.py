@@ -58,7 +58,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     if not force and not _stale(LIB, deps):
         return LIB
     os.makedirs(OBJ, exist_ok=True)
-    units = [(os.path.join(CSRC, "btd.cu"), [], os.path.join(OBJ, "btd.o"))]
+    units = [(os.path.join(CSRC, "btd.cu"), [], os.path.join(OBJ, "btd.o")),
+             (os.path.join(CSRC, "btd_persist.cu"), [], os.path.join(OBJ, "btd_persist.o"))]
     for dt in DTYPES:
         for nb in SIZES:
             units.append((os.path.join(CSRC, "btd_inst.cu"), [f"-DBTD_T={dt}", f"-DBTD_NB={nb}"],

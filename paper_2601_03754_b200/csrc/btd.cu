@@ -12,6 +12,7 @@
 #include <new>
 
 #include "btd_internal.h"
+#include "btd_persist.cuh"
 
 using namespace btd;
 
@@ -59,6 +60,10 @@ static size_t fused_bytes_dt(const btd_plan *p, bool fact, bool solve) {
 static btd_status run(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
                       void *x, int32_t *info, int64_t sys0, int64_t count, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (p->variant == BTD_VARIANT_PERSIST) {
+        if (p->dtype == BTD_F32) return run_persist<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+        return run_persist<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    }
     if (p->dtype == BTD_F32) return run_dtype<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
     return run_dtype<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
 }
@@ -72,8 +77,10 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
     *out = nullptr;
     if (N < 1 || n < 1 || batch < 1 || m < 1 || (dtype != BTD_F32 && dtype != BTD_F64)) return BTD_EINVAL;
     if (N > (1ll << 24) || m > 4096) return BTD_EINVAL;
-    const int NB = pick_nb(n);
-    if (NB < 0) return BTD_EUNSUPPORTED;
+    if (n > 128) return BTD_EUNSUPPORTED;
+    if (variant < BTD_VARIANT_AUTO || variant > BTD_VARIANT_PERSIST) return BTD_EINVAL;
+    const int NB = pick_nb(n);  // -1 for n > 32: only PERSIST handles those
+    if (NB < 0 && (variant == BTD_VARIANT_FUSED || variant == BTD_VARIANT_LEVEL)) return BTD_EUNSUPPORTED;
     btd_plan *p = new (std::nothrow) btd_plan();
     if (!p) return BTD_ENOMEM;
     p->N = N; p->n = n; p->batch = batch; p->m = m; p->dtype = dtype; p->NB = NB;
@@ -89,16 +96,24 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
     }
     p->geo.nC = off;
     const bool f32 = dtype == BTD_F32;
-    p->smem_fs = f32 ? fused_bytes_dt<float>(p, true, true) : fused_bytes_dt<double>(p, true, true);
-    p->smem_f = f32 ? fused_bytes_dt<float>(p, true, false) : fused_bytes_dt<double>(p, true, false);
-    p->smem_s = f32 ? fused_bytes_dt<float>(p, false, true) : fused_bytes_dt<double>(p, false, true);
+    if (NB > 0) {
+        p->smem_fs = f32 ? fused_bytes_dt<float>(p, true, true) : fused_bytes_dt<double>(p, true, true);
+        p->smem_f = f32 ? fused_bytes_dt<float>(p, true, false) : fused_bytes_dt<double>(p, true, false);
+        p->smem_s = f32 ? fused_bytes_dt<float>(p, false, true) : fused_bytes_dt<double>(p, false, true);
+    } else {
+        p->smem_fs = p->smem_f = p->smem_s = ~(size_t)0;
+    }
+    const size_t psm = f32 ? PersistSmem<float>::bytes((int)n, (int)m) : PersistSmem<double>::bytes((int)n, (int)m);
     const bool fits = p->smem_fs <= kMaxSmem;
-    if (variant == BTD_VARIANT_FUSED && !fits) {
+    if ((variant == BTD_VARIANT_FUSED && !fits) || (variant == BTD_VARIANT_PERSIST && psm > kMaxSmem)) {
         delete p;
         return BTD_EUNSUPPORTED;
     }
-    p->variant = (variant == BTD_VARIANT_LEVEL || (variant == BTD_VARIANT_AUTO && !fits)) ? BTD_VARIANT_LEVEL
-                                                                                           : BTD_VARIANT_FUSED;
+    if (variant == BTD_VARIANT_AUTO)
+        p->variant = fits ? BTD_VARIANT_FUSED : BTD_VARIANT_PERSIST;
+    else
+        p->variant = variant;
+    p->smem_persist = psm;
     *out = p;
     return BTD_OK;
 }
@@ -132,7 +147,7 @@ int32_t btd_plan_variant(const btd_plan *p) { return p ? p->variant : -1; }
 
 int32_t btd_plan_launches(const btd_plan *p, int32_t op) {
     if (!p || op < 0 || op > 2) return -1;
-    if (p->variant == BTD_VARIANT_FUSED) return 1;
+    if (p->variant == BTD_VARIANT_FUSED || p->variant == BTD_VARIANT_PERSIST) return 1;
     const int64_t chunks = (p->batch + 65534) / 65535;
     const int per = op == 0 ? p->L : op == 1 ? 2 * p->L : 2 * p->L;
     return (int32_t)(1 + chunks * per);
@@ -140,6 +155,7 @@ int32_t btd_plan_launches(const btd_plan *p, int32_t op) {
 
 int64_t btd_plan_smem_bytes(const btd_plan *p) {
     if (!p) return -1;
+    if (p->variant == BTD_VARIANT_PERSIST) return (int64_t)p->smem_persist;
     return p->variant == BTD_VARIANT_FUSED ? (int64_t)p->smem_fs : 0;
 }
 

@@ -12,6 +12,7 @@ struct btd_plan {
     int NB;        // compiled block size
     int variant;   // BTD_VARIANT_FUSED / BTD_VARIANT_LEVEL
     size_t smem_fs, smem_f, smem_s;  // fused smem bytes: factor+solve, factor, solve
+    size_t smem_persist;             // PERSIST kernel dynamic smem bytes
     btd::Geo geo;
 };
 
@@ -40,6 +41,11 @@ size_t fused_bytes(const btd_plan *p, bool fact, bool solve) {
     if (FusedRCfg<T, NB>::OK) return FusedRCfg<T, NB>::bytes((int)p->N, (int)p->m, fact, solve);
     return FusedSmem<T, NB, FusedCfg<T, NB>::NT>::bytes((int)p->N, (int)p->m, fact, solve);
 }
+
+// Defined in btd_persist.cu (any n <= 128, cooperative launch).
+template <typename T>
+btd_status run_persist(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
+                       void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st);
 
 // Defined in btd_inst.cu, explicitly instantiated once per (T, NB) translation unit.
 template <typename T, int NB>

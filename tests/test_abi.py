@@ -58,11 +58,15 @@ def test_plan_matches_oracle_definitions(N):
 def test_variant_selection():
     # c5 (n=12, N=128, fp32) fits one SM's shared memory -> fused; c3 (n=32, N=1024) does not
     assert btd.Plan(128, 12, 8192, 1, torch.float32).variant == "fused"
-    assert btd.Plan(1024, 32, 1, 1, torch.float64).variant == "level"
+    assert btd.Plan(1024, 32, 1, 1, torch.float64).variant == "persist"
+    assert btd.Plan(256, 128, 1, 1, torch.float64).variant == "persist"
     assert btd.Plan(64, 16, 1, 1, torch.float64).variant == "fused"
     assert btd.Plan(8, 2, 1, 1, torch.float64).launches() == 1
-    p = btd.Plan(1024, 32, 1, 1, torch.float64)
+    assert btd.Plan(1024, 32, 1, 1, torch.float64).launches() == 1
+    p = btd.Plan(1024, 32, 1, 1, torch.float64, variant="level")
     assert p.launches("factor_solve") == 1 + 2 * p.levels
+    with pytest.raises(btd.BtdError):
+        btd.Plan(256, 64, 1, 1, torch.float64, variant="level")
     with pytest.raises(btd.BtdError):
         btd.Plan(4096, 32, 1, 1, torch.float64, variant="fused")
 
