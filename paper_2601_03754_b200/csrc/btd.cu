@@ -60,7 +60,7 @@ static size_t fused_bytes_dt(const btd_plan *p, bool fact, bool solve) {
 static btd_status run(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
                       void *x, int32_t *info, int64_t sys0, int64_t count, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (p->variant == BTD_VARIANT_PERSIST) {
+    if (p->variant == BTD_VARIANT_PERSIST && p->NB < 0) {  // n > 32: CTA-wide block ops
         if (p->dtype == BTD_F32) return run_persist<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
         return run_persist<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
     }
@@ -103,7 +103,7 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
     } else {
         p->smem_fs = p->smem_f = p->smem_s = ~(size_t)0;
     }
-    const size_t psm = f32 ? PersistSmem<float>::bytes((int)n, (int)m) : PersistSmem<double>::bytes((int)n, (int)m);
+    const size_t psm = NB > 0 ? 0 : (f32 ? PersistSmem<float>::bytes((int)n, (int)m) : PersistSmem<double>::bytes((int)n, (int)m));
     const bool fits = p->smem_fs <= kMaxSmem;
     if ((variant == BTD_VARIANT_FUSED && !fits) || (variant == BTD_VARIANT_PERSIST && psm > kMaxSmem)) {
         delete p;

@@ -1,6 +1,7 @@
 // btd_inst.cu -- typed launchers; compiled once per (dtype, NB) with -DBTD_T=<float|double> -DBTD_NB=<n>
 // so the 20 instantiations build in parallel (see paper_2601_03754_b200/build.py).
 #include "btd_internal.h"
+#include "btd_persist.cuh"
 
 namespace btd {
 static btd_status cuda_fail(cudaError_t e) { return record_cuda_error(e); }
@@ -89,11 +90,55 @@ static btd_status launch_level(const btd_plan *p, const T *D, const T *E, const 
     return BTD_OK;
 }
 
+template <typename T, int NB, bool FACT, bool SOLVE>
+static btd_status launch_persist_team(const btd_plan *p, const T *D, const T *E, const T *b, T *Dhat, T *C, T *x,
+                                      int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    using Cfg = PTeamCfg<T, NB>;
+    auto kern = btd_persist_team_kernel<T, NB, FACT, SOLVE>;
+    const size_t smem = Cfg::BYTES;
+    static size_t attr_bytes = 0;
+    if (smem > 48 * 1024 && smem > attr_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_fail(e);
+        attr_bytes = smem;
+    }
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (per_sm < 1) return BTD_EUNSUPPORTED;
+    const int64_t N = p->N, n = p->n, m = p->m;
+    const size_t nn = (size_t)n * n;
+    const T *Dt = FACT ? D + sys0 * N * nn : nullptr;
+    const T *Et = (FACT && E) ? E + sys0 * (size_t)(N - 1) * nn : nullptr;
+    const T *bt = SOLVE ? b + sys0 * (size_t)N * n * m : nullptr;
+    T *Dh = Dhat + sys0 * N * nn;
+    T *Ct = C + sys0 * (size_t)p->geo.nC * nn;
+    T *xt = SOLVE ? x + sys0 * (size_t)N * n * m : nullptr;
+    int32_t *inf = FACT ? info + sys0 : nullptr;
+    Geo g = p->geo;
+    int batch = (int)count;
+    const long long want = ((long long)count * ((N + 1) / 2) + Cfg::NT - 1) / Cfg::NT;
+    const long long maxg = (long long)nsm * per_sm;
+    int grid = (int)(want < maxg ? (want > 0 ? want : 1) : maxg);
+    void *args[] = {(void *)&Dt, (void *)&Et, (void *)&bt, (void *)&Dh, (void *)&Ct,
+                    (void *)&xt, (void *)&inf, (void *)&g, (void *)&batch};
+    e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(Cfg::THREADS), args, smem, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    return BTD_OK;
+}
+
 template <typename T, int NB>
 btd_status run_typed(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat,
                             void *C, void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
     const T *Dt = (const T *)D, *Et = (const T *)E, *bt = (const T *)b;
     T *Dh = (T *)Dhat, *Ct = (T *)C, *xt = (T *)x;
+    if (p->variant == BTD_VARIANT_PERSIST) {
+        if (op == 0) return launch_persist_team<T, NB, true, false>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+        if (op == 1) return launch_persist_team<T, NB, false, true>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+        return launch_persist_team<T, NB, true, true>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
+    }
     if (p->variant == BTD_VARIANT_FUSED) {
         if (op == 0) return launch_fused<T, NB, true, false>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);
         if (op == 1) return launch_fused<T, NB, false, true>(p, Dt, Et, bt, Dh, Ct, xt, info, sys0, count, st);

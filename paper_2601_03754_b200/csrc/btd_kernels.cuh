@@ -658,6 +658,11 @@ __global__ void btd_level_init_kernel(const T *__restrict__ D, const T *__restri
         for (long long q = t0; q < nb; q += stride) x[q] = bvec[q];
 }
 
+template <int NB>
+struct LevelShape_TS {
+    static constexpr int TS = NB <= 1 ? 1 : NB <= 2 ? 2 : NB <= 4 ? 4 : NB <= 8 ? 8 : NB <= 16 ? 16 : 32;
+};
+
 // One level l of Alg. 4 (FACT) and/or the forward sweep of Alg. 6 (SOLVE), deferred form.
 // grid = (ceil(ncols / NT), batch); one team (one row per lane) per column; dynamic smem NT * TSTR.
 template <typename T, int NB>
@@ -666,33 +671,31 @@ struct LevelSmem {
     static constexpr int TSTR = 3 * BLK + 64 / (int)sizeof(T);
 };
 
-template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE>
-__global__ void __launch_bounds__(NT *TS) btd_level_fwd_kernel(const T *__restrict__ E, T *Dhat, T *C, T *x,
-                                                              int32_t *info, Geo g, int l, int sys0) {
+// One column op of level l for (system sys, column index j): the body shared by the LEVEL kernel
+// (one launch per level) and the PERSIST-TEAM kernel (one cooperative launch, grid.sync per level).
+// `scr` is this team's shared-memory scratch (LevelSmem::TSTR elements). Warp-collective.
+template <typename T, int NB, int TS, bool FACT, bool SOLVE>
+__device__ __forceinline__ void level_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int32_t *info,
+                                               const Geo &g, int l, long long sys, int j, T *scr) {
     constexpr int LD = Dims<T, NB>::LD, BLK = Dims<T, NB>::BLK;
     constexpr int RPL = 1;
-    extern __shared__ __align__(16) unsigned char lsm_raw[];
-    T *scr_all = reinterpret_cast<T *>(lsm_raw);
-
     const int N = g.N, n = g.n, m = g.m;
-    const long long sys = (long long)blockIdx.y + sys0;
     const size_t nn = (size_t)n * n;
     const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
     T *Dh = Dhat + sys * N * nn;
     T *Cs = C + sys * (size_t)g.nC * nn;
     T *xs = x ? x + sys * (size_t)N * n * m : nullptr;
 
-    const int tid = threadIdx.x, lane = tid & 31, team = tid / TS;
+    const int lane = threadIdx.x & 31;
     Lane<NB, TS> ln{lane % TS, lane - lane % TS};
     const int r = ln.q;
     const bool rv = ln.valid(0);
-    T *sLt = scr_all + team * LevelSmem<T, NB>::TSTR;
+    T *sLt = scr;
     T *sB = sLt + BLK;  // right coupling rows / deferred coupling rows / y broadcast
     T *sCl = sB + BLK;  // left coupling, row-major
 
     const int s = 1 << (l - 1);
     const int ncols = ((N / s) + 1) / 2;
-    const int j = blockIdx.x * NT + team;
     const bool act = j < ncols;
     const int c = act ? s * (2 * j + 1) : s;
     const bool hasL = act && c > s;
@@ -814,25 +817,32 @@ __global__ void __launch_bounds__(NT *TS) btd_level_fwd_kernel(const T *__restri
     }
 }
 
-// Backward sweep level l (Alg. 6 lines 10-16): x_c = D^_c^{-T}(y_c - C_r^T x_{c+s} - C_l x_{c-s}).
-template <typename T, int NB, int TS, int NT>
-__global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, const T *C, T *x, Geo g, int l,
-                                                              int sys0) {
+template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE>
+__global__ void __launch_bounds__(NT *TS) btd_level_fwd_kernel(const T *__restrict__ E, T *Dhat, T *C, T *x,
+                                                              int32_t *info, Geo g, int l, int sys0) {
+    extern __shared__ __align__(16) unsigned char lsm_raw[];
+    T *scr = reinterpret_cast<T *>(lsm_raw) + (threadIdx.x / TS) * LevelSmem<T, NB>::TSTR;
+    level_fwd_task<T, NB, TS, FACT, SOLVE>(E, Dhat, C, x, info, g, l, (long long)blockIdx.y + sys0,
+                                           blockIdx.x * NT + (int)(threadIdx.x / TS), scr);
+}
+
+// Backward sweep of one column (Alg. 6 lines 10-16): x_c = D^_c^{-T}(y_c - C_r^T x_{c+s} - C_l x_{c-s}).
+// sx: 2*NB elements of this team's shared scratch. Warp-collective.
+template <typename T, int NB, int TS>
+__device__ __forceinline__ void level_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int l, long long sys,
+                                               int j, T *sxs) {
     constexpr int RPL = 1;
-    __shared__ __align__(16) T sx[NT][2][NB];
     const int N = g.N, n = g.n, m = g.m;
-    const long long sys = (long long)blockIdx.y + sys0;
     const size_t nn = (size_t)n * n;
     const T *Dh = Dhat + sys * N * nn;
     const T *Cs = C + sys * (size_t)g.nC * nn;
     T *xs = x + sys * (size_t)N * n * m;
-    const int tid = threadIdx.x, lane = tid & 31, team = tid / TS;
+    const int lane = threadIdx.x & 31;
     Lane<NB, TS> ln{lane % TS, lane - lane % TS};
     const int r = ln.q;
     const bool rv = ln.valid(0);
     const int s = 1 << (l - 1);
     const int ncols = ((N / s) + 1) / 2;
-    const int j = blockIdx.x * NT + team;
     const bool act = j < ncols;
     const int c = act ? s * (2 * j + 1) : s;
     const bool hasL = act && c > s;
@@ -846,8 +856,8 @@ __global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, co
     for (int k = 0; k < NB; ++k) dinv[0] = (k == r) ? rcp_rn(lc[0][k]) : dinv[0];
     for (int q = 0; q < m; ++q) {
         if (rv) {
-            sx[team][0][r] = (hasR && r < n) ? xs[((size_t)(c + s - 1) * n + r) * m + q] : T(0);
-            sx[team][1][r] = (hasL && r < n) ? xs[((size_t)(c - s - 1) * n + r) * m + q] : T(0);
+            sxs[r] = (hasR && r < n) ? xs[((size_t)(c + s - 1) * n + r) * m + q] : T(0);
+            sxs[NB + r] = (hasL && r < n) ? xs[((size_t)(c - s - 1) * n + r) * m + q] : T(0);
         }
         __syncwarp();
         T v[RPL];
@@ -855,8 +865,8 @@ __global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, co
         T a = T(0), b2 = T(0);
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            a = fma(crc[0][k], sx[team][0][k], a);
-            b2 = fma(clr[0][k], sx[team][1][k], b2);
+            a = fma(crc[0][k], sxs[k], a);
+            b2 = fma(clr[0][k], sxs[NB + k], b2);
         }
         v[0] -= a;
         v[0] -= b2;
@@ -864,6 +874,14 @@ __global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, co
         if (act && r < n) xs[((size_t)(c - 1) * n + r) * m + q] = v[0];
         __syncwarp();
     }
+}
+
+template <typename T, int NB, int TS, int NT>
+__global__ void __launch_bounds__(NT *TS) btd_level_bwd_kernel(const T *Dhat, const T *C, T *x, Geo g, int l,
+                                                              int sys0) {
+    __shared__ __align__(16) T sx[NT][2 * NB];
+    level_bwd_task<T, NB, TS>(Dhat, C, x, g, l, (long long)blockIdx.y + sys0, blockIdx.x * NT + (int)(threadIdx.x / TS),
+                              sx[threadIdx.x / TS]);
 }
 
 }  // namespace btd

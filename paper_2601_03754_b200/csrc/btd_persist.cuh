@@ -467,3 +467,75 @@ __global__ void __launch_bounds__(kPThreads, 1)
 }
 
 }  // namespace btd
+
+namespace btd {
+
+// ---------------------------------------------------------------- PERSIST-TEAM (n <= 32)
+//
+// Same dataflow as the LEVEL variant (Alg. 4 deferred form, one column op per team of lanes,
+// state in the output buffers) but in ONE cooperative launch: tasks (system, column) of level l
+// are spread over every team of every resident CTA and levels are separated by grid.sync(),
+// so there is one launch per call instead of 2L+1 and the instruction stream stays warm.
+template <typename T, int NB>
+struct PTeamCfg {
+    static constexpr int TS = LevelShape_TS<NB>::TS;
+    static constexpr int THREADS = 256;
+    static constexpr int NT = THREADS / TS;
+    static constexpr int TSTR = LevelSmem<T, NB>::TSTR;
+    static constexpr size_t BYTES = (size_t)NT * TSTR * sizeof(T);
+};
+
+template <typename T, int NB, bool FACT, bool SOLVE>
+__global__ void __launch_bounds__(PTeamCfg<T, NB>::THREADS, 1)
+    btd_persist_team_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat,
+                            T *C, T *x, int32_t *info, Geo g, int batch) {
+    using Cfg = PTeamCfg<T, NB>;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char ptsm_raw[];
+    const int team = threadIdx.x / Cfg::TS;
+    T *scr = reinterpret_cast<T *>(ptsm_raw) + (size_t)team * Cfg::TSTR;
+    const long long gteam = (long long)blockIdx.x * Cfg::NT + team;
+    const long long nteams = (long long)gridDim.x * Cfg::NT;
+    {   // a1: Dhat <- D, x <- b, info <- 0
+        const size_t stride = (size_t)gridDim.x * blockDim.x;
+        const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const size_t nD = (size_t)batch * g.N * g.n * g.n, nb = (size_t)batch * g.N * g.n * g.m;
+        if (FACT) {
+            if (D != Dhat)
+                for (size_t q = t0; q < nD; q += stride) Dhat[q] = D[q];
+            for (size_t q = t0; q < (size_t)batch; q += stride) info[q] = 0;
+        }
+        if (SOLVE && bvec != x)
+            for (size_t q = t0; q < nb; q += stride) x[q] = bvec[q];
+        grid.sync();
+    }
+    for (int l = 1; l <= g.L; ++l) {
+        const int ncols = ((g.N >> (l - 1)) + 1) / 2;
+        const long long ntask = (long long)batch * ncols;
+        // all lanes of a warp iterate together (teams of one warp share the loop trip count)
+        const long long first = gteam - (gteam % (32 / Cfg::TS));
+        for (long long t0 = first; t0 < ntask; t0 += nteams) {
+            const long long task = t0 + (gteam - first);
+            const long long sys = task < ntask ? task / ncols : 0;
+            const int j = task < ntask ? (int)(task % ncols) : ncols;  // j >= ncols: inactive team
+            level_fwd_task<T, NB, Cfg::TS, FACT, SOLVE>(E, Dhat, C, x, info, g, l, sys, j, scr);
+        }
+        grid.sync();
+    }
+    if (SOLVE) {
+        for (int l = g.L; l >= 1; --l) {
+            const int ncols = ((g.N >> (l - 1)) + 1) / 2;
+            const long long ntask = (long long)batch * ncols;
+            const long long first = gteam - (gteam % (32 / Cfg::TS));
+            for (long long t0 = first; t0 < ntask; t0 += nteams) {
+                const long long task = t0 + (gteam - first);
+                const long long sys = task < ntask ? task / ncols : 0;
+                const int j = task < ntask ? (int)(task % ncols) : ncols;
+                level_bwd_task<T, NB, Cfg::TS>(Dhat, C, x, g, l, sys, j, scr);
+            }
+            grid.sync();
+        }
+    }
+}
+
+}  // namespace btd
