@@ -53,7 +53,13 @@ def _compile(args: tuple[str, list[str], str]) -> str:
     return (r.stderr or "").strip()
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, timing: bool = False) -> str:
+    """Compile libbtd.so (timing=True: libbtd_timing.so with -DBTD_TIMING phase counters, dev tool)."""
+    global LIB, OBJ, FLAGS
+    if timing:
+        LIB = os.path.join(HERE, "libbtd_timing.so")
+        OBJ = os.path.join(HERE, "build_timing")
+        FLAGS = FLAGS + ["-DBTD_TIMING"]
     deps = _sources()
     if not force and not _stale(LIB, deps):
         return LIB
@@ -76,4 +82,4 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, timing="--timing" in sys.argv))

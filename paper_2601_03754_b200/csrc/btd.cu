@@ -13,6 +13,7 @@
 
 #include "btd_internal.h"
 #include "btd_persist.cuh"
+#include "btd_wide.cuh"
 
 using namespace btd;
 
@@ -60,6 +61,10 @@ static size_t fused_bytes_dt(const btd_plan *p, bool fact, bool solve) {
 static btd_status run(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
                       void *x, int32_t *info, int64_t sys0, int64_t count, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (p->variant == BTD_VARIANT_WIDE) {
+        if (p->dtype == BTD_F32) return run_wide<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+        return run_wide<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    }
     if (p->variant == BTD_VARIANT_PERSIST && p->NB < 0) {  // n > 32: CTA-wide block ops
         if (p->dtype == BTD_F32) return run_persist<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
         return run_persist<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
@@ -78,9 +83,10 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
     if (N < 1 || n < 1 || batch < 1 || m < 1 || (dtype != BTD_F32 && dtype != BTD_F64)) return BTD_EINVAL;
     if (N > (1ll << 24) || m > 4096) return BTD_EINVAL;
     if (n > 128) return BTD_EUNSUPPORTED;
-    if (variant < BTD_VARIANT_AUTO || variant > BTD_VARIANT_PERSIST) return BTD_EINVAL;
+    if (variant < BTD_VARIANT_AUTO || variant > BTD_VARIANT_WIDE) return BTD_EINVAL;
     const int NB = pick_nb(n);  // -1 for n > 32: only PERSIST handles those
-    if (NB < 0 && (variant == BTD_VARIANT_FUSED || variant == BTD_VARIANT_LEVEL)) return BTD_EUNSUPPORTED;
+    if (NB < 0 && (variant == BTD_VARIANT_FUSED || variant == BTD_VARIANT_LEVEL || variant == BTD_VARIANT_WIDE))
+        return BTD_EUNSUPPORTED;
     btd_plan *p = new (std::nothrow) btd_plan();
     if (!p) return BTD_ENOMEM;
     p->N = N; p->n = n; p->batch = batch; p->m = m; p->dtype = dtype; p->NB = NB;
@@ -109,10 +115,18 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         delete p;
         return BTD_EUNSUPPORTED;
     }
-    if (variant == BTD_VARIANT_AUTO)
-        p->variant = fits ? BTD_VARIANT_FUSED : BTD_VARIANT_PERSIST;
-    else
+    const size_t wsm = f32 ? WideSmem<float>::bytes((int)n, (int)m) : WideSmem<double>::bytes((int)n, (int)m);
+    if (variant == BTD_VARIANT_WIDE && wsm > kMaxSmem) {
+        delete p;
+        return BTD_EUNSUPPORTED;
+    }
+    if (variant == BTD_VARIANT_AUTO) {
+        // few independent systems with enough level-1 columns to spread over the SMs: latency path
+        const bool wide_ok = NB > 0 && wsm <= kMaxSmem && batch * ((N + 1) / 2) <= 4 * 148 && N >= 16;
+        p->variant = wide_ok ? BTD_VARIANT_WIDE : fits ? BTD_VARIANT_FUSED : BTD_VARIANT_PERSIST;
+    } else {
         p->variant = variant;
+    }
     p->smem_persist = psm;
     *out = p;
     return BTD_OK;
@@ -147,7 +161,7 @@ int32_t btd_plan_variant(const btd_plan *p) { return p ? p->variant : -1; }
 
 int32_t btd_plan_launches(const btd_plan *p, int32_t op) {
     if (!p || op < 0 || op > 2) return -1;
-    if (p->variant == BTD_VARIANT_FUSED || p->variant == BTD_VARIANT_PERSIST) return 1;
+    if (p->variant != BTD_VARIANT_LEVEL) return 1;
     const int64_t chunks = (p->batch + 65534) / 65535;
     const int per = op == 0 ? p->L : op == 1 ? 2 * p->L : 2 * p->L;
     return (int32_t)(1 + chunks * per);

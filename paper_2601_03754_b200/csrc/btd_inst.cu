@@ -150,6 +150,20 @@ btd_status run_typed(const btd_plan *p, int op, const void *D, const void *E, co
 }
 
 
+#if defined(BTD_TIMING) && defined(BTD_NB) && BTD_NB == 12
+}  // namespace btd
+#define BTD_CAT2(a, b) a##b
+#define BTD_CAT(a, b) BTD_CAT2(a, b)
+extern "C" int BTD_CAT(btd_debug_timing_, BTD_T)(unsigned long long *host16, int reset) {
+    if (reset) {
+        unsigned long long z[16] = {0};
+        return (int)cudaMemcpyToSymbol(btd::btd_timing, z, sizeof z);
+    }
+    return (int)cudaMemcpyFromSymbol(host16, btd::btd_timing, 16 * sizeof(unsigned long long));
+}
+namespace btd {
+#endif
+
 #if defined(BTD_T) && defined(BTD_NB)
 template btd_status run_typed<BTD_T, BTD_NB>(const btd_plan *, int, const void *, const void *, const void *,
                                              void *, void *, void *, int32_t *, int64_t, int64_t, cudaStream_t);

@@ -47,6 +47,11 @@ template <typename T>
 btd_status run_persist(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
                        void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st);
 
+// Defined in btd_persist.cu (n <= 32, one CTA per column op, cooperative launch).
+template <typename T>
+btd_status run_wide(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
+                    void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st);
+
 // Defined in btd_inst.cu, explicitly instantiated once per (T, NB) translation unit.
 template <typename T, int NB>
 btd_status run_typed(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,

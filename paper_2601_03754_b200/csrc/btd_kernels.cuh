@@ -31,6 +31,8 @@
 //
 // Indices: original blocks are 1-based; slot (l, k) of C is at off[l-1] + k - 1 (include/btd.h).
 #pragma once
+#include <cuda_pipeline.h>
+
 #include "btd_team.cuh"
 
 namespace btd {
@@ -42,6 +44,28 @@ struct Geo {
 };
 
 __device__ __forceinline__ long long cslot(const Geo &g, int l, int k) { return g.off[l - 1] + k - 1; }
+
+// Optional phase timing (build with -DBTD_TIMING): CTA 0 accumulates clock64() deltas per phase id
+// into btd_timing[] (read back with cudaMemcpyFromSymbol by tools/phase_times.py).
+#ifdef BTD_TIMING
+static __device__ unsigned long long btd_timing[16];
+#define BTD_STAMP(id)                                                         \
+    do {                                                                      \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                            \
+            const unsigned long long now_ = clock64();                        \
+            btd_timing[(id)] += now_ - btd_t_last;                            \
+            btd_t_last = now_;                                                \
+        }                                                                     \
+    } while (0)
+#define BTD_STAMP_INIT() unsigned long long btd_t_last = clock64()
+#else
+#define BTD_STAMP(id) \
+    do {              \
+    } while (0)
+#define BTD_STAMP_INIT() \
+    do {                 \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------------------- shared pieces
 
@@ -56,10 +80,12 @@ __device__ __forceinline__ void fused_load_inputs(T *slots, T *Y, const T *Ds, c
             constexpr int W = VecT<T>::W;
             const size_t tot = (size_t)N * nn;
             if (tot % W == 0) {
+                // asynchronous 16-byte copies (LDGSTS): every thread keeps all of its loads in flight
                 using V = typename VecT<T>::type;
                 const V *src = reinterpret_cast<const V *>(Ds);
                 V *dst = reinterpret_cast<V *>(slots);
-                for (size_t q = tid; q < tot / W; q += blockDim.x) dst[q] = src[q];
+                for (size_t q = tid; q < tot / W; q += blockDim.x) __pipeline_memcpy_async(dst + q, src + q, 16);
+                __pipeline_commit();
             } else {
                 for (size_t q = tid; q < tot; q += blockDim.x) slots[q] = Ds[q];
             }
@@ -76,12 +102,20 @@ __device__ __forceinline__ void fused_load_inputs(T *slots, T *Y, const T *Ds, c
         }
     }
     if (SOLVE) {
-        for (size_t q = tid; q < (size_t)N * m * LD; q += blockDim.x) {
-            const int i = (int)(q / ((size_t)m * LD)), rem = (int)(q % ((size_t)m * LD));
-            const int qq = rem / LD, r2 = rem % LD;
-            Y[q] = (r2 < n) ? bs[((size_t)i * n + r2) * m + qq] : T(0);
+        if (m == 1 && n == LD && ((size_t)N * n) % VecT<T>::W == 0) {
+            using V = typename VecT<T>::type;
+            for (size_t q = tid; q < (size_t)N * n / VecT<T>::W; q += blockDim.x)
+                __pipeline_memcpy_async(reinterpret_cast<V *>(Y) + q, reinterpret_cast<const V *>(bs) + q, 16);
+            __pipeline_commit();
+        } else {
+            for (size_t q = tid; q < (size_t)N * m * LD; q += blockDim.x) {
+                const int i = (int)(q / ((size_t)m * LD)), rem = (int)(q % ((size_t)m * LD));
+                const int qq = rem / LD, r2 = rem % LD;
+                Y[q] = (r2 < n) ? bs[((size_t)i * n + r2) * m + qq] : T(0);
+            }
         }
     }
+    __pipeline_wait_prior(0);
 }
 
 template <typename T, int NB>
@@ -131,8 +165,8 @@ __device__ __forceinline__ int team_potrf_full(T (&a)[RPL][NB], T (&Lf)[NB][NB],
     for (int k = 0; k < NB; ++k) {
         const T akk = __shfl_sync(kFull, a[k / TS][k], ln.base + k % TS);
         bad = (!(akk > T(0)) && bad < 0) ? k : bad;
-        const T d = sqrt_rn(akk);
-        const T inv = rcp_rn(d);
+        T d, inv;
+        pivot(akk, d, inv);
         Lf[k][k] = d;
         Linv[k] = inv;
 #pragma unroll
@@ -194,7 +228,7 @@ __device__ __forceinline__ void load_L_full(T (&Lf)[NB][NB], T (&Linv)[NB], cons
         g_load_row1<T, NB>(row, blk, n, i, true, true);
 #pragma unroll
         for (int k = 0; k <= i; ++k) Lf[i][k] = row[k];
-        Linv[i] = rcp_rn(row[i]);
+        Linv[i] = rcp_fast(row[i]);
     }
 }
 
@@ -221,10 +255,12 @@ __global__ void __launch_bounds__(NT *TS, 2)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, team = tid / TS;
     Lane<NB, TS> ln{lane % TS, lane - lane % TS};
 
+    BTD_STAMP_INIT();
     if (tid == 0) s_fail = 0xffffffffu;
     fused_load_inputs<T, NB, FACT, SOLVE>(slots, Y, D ? D + sys * N * nn : nullptr,
                                           SOLVE ? bvec + sys * (size_t)N * n * m : nullptr, N, n, m);
     __syncthreads();
+    BTD_STAMP(0);
 
     for (int l = 1; l <= g.L; ++l) {
         const int s = 1 << (l - 1);
@@ -243,6 +279,11 @@ __global__ void __launch_bounds__(NT *TS, 2)
                 T Lf[NB][NB], Linv[NB];
                 T cr[RPL][NB];
                 if (FACT) {
+                    // level-1 couplings come from HBM: issue those loads before the POTRF chain
+                    if (l == 1) {
+                        g_load_rows<T, NB, TS, RPL>(cr, Es + (size_t)(c - 1) * nn, n, ln, hasR, false);
+                        g_load_cols<T, NB, TS, RPL>(cl, Es + (size_t)((c >= 2 ? c : 2) - 2) * nn, n, ln, hasL, false);
+                    }
                     // -- a3: D~_c -> D^_c
                     T a[RPL][NB];
                     s_load_rows<T, NB, TS, RPL>(a, slots + (size_t)(c - 1) * BLK, ln);
@@ -251,10 +292,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                     if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
                     g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
                     // -- a4: couplings (row q+TS t of the right one, column q+TS t of the left one)
-                    if (l == 1) {
-                        g_load_rows<T, NB, TS, RPL>(cr, Es + (size_t)(c - 1) * nn, n, ln, hasR, false);
-                        g_load_cols<T, NB, TS, RPL>(cl, Es + (size_t)((c >= 2 ? c : 2) - 2) * nn, n, ln, hasL, false);
-                    } else {
+                    if (l != 1) {
                         s_load_rows<T, NB, TS, RPL>(cr, slots + (size_t)((hasR ? c + s / 2 : c) - 1) * BLK, ln);
                         s_load_cols<T, NB, TS, RPL>(cl, slots + (size_t)((hasL ? c - s / 2 : c) - 1) * BLK, ln);
 #pragma unroll
@@ -341,6 +379,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                 }
             }
             __syncthreads();
+            BTD_STAMP(l < 11 ? 5 + l : 1);
             // ---- phase Y: left pushes (deferred left-looking part of Alg. 4, l.7/l.9)
             if (wact && hasL) {
                 if (FACT) {
@@ -364,6 +403,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                 }
             }
             __syncthreads();
+            BTD_STAMP(2);
         }
     }
 
@@ -415,8 +455,11 @@ __global__ void __launch_bounds__(NT *TS, 2)
                 }
             }
             __syncthreads();
+            BTD_STAMP(3);
         }
         fused_store_x<T, NB>(x + sys * (size_t)N * n * m, Y, N, n, m);
+        __syncthreads();
+        BTD_STAMP(4);
     }
     if (FACT && tid == 0) info[sys] = (s_fail == 0xffffffffu) ? 0 : (int)(s_fail & ((1u << 25) - 1));
 }

@@ -1,6 +1,7 @@
 // btd_persist.cu -- launcher of the PERSIST variant (cooperative launch, one kernel per call).
 #include "btd_internal.h"
 #include "btd_persist.cuh"
+#include "btd_wide.cuh"
 
 namespace btd {
 
@@ -43,6 +44,57 @@ btd_status run_persist(const btd_plan *p, int op, const void *D, const void *E, 
     if (e != cudaSuccess) return record_cuda_error(e);
     return BTD_OK;
 }
+
+template <typename T, int NB>
+static btd_status launch_wide(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat,
+                              void *C, void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    const int n = (int)p->n, m = (int)p->m, N = (int)p->N;
+    const size_t smem = WideSmem<T>::bytes(n, m);
+    auto kern = btd_wide_kernel<T, NB>;
+    static size_t attr_bytes = 0;
+    if (smem > 48 * 1024 && smem > attr_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return record_cuda_error(e);
+        attr_bytes = smem;
+    }
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWThreads, smem);
+    if (e != cudaSuccess) return record_cuda_error(e);
+    if (per_sm < 1) return BTD_EUNSUPPORTED;
+    const size_t nn = (size_t)n * n;
+    const T *Dt = op != 1 ? (const T *)D + sys0 * N * nn : nullptr;
+    const T *Et = E ? (const T *)E + sys0 * (size_t)(N - 1) * nn : nullptr;
+    const T *bt = b ? (const T *)b + sys0 * (size_t)N * n * m : nullptr;
+    T *Dh = (T *)Dhat + sys0 * N * nn;
+    T *Ct = (T *)C + sys0 * (size_t)p->geo.nC * nn;
+    T *xt = x ? (T *)x + sys0 * (size_t)N * n * m : nullptr;
+    int32_t *inf = info ? info + sys0 : nullptr;
+    Geo g = p->geo;
+    int batch = (int)count, fact = op != 1, solve = op != 0;
+    const long long want = (long long)count * ((N + 1) / 2);
+    const long long maxg = (long long)nsm * per_sm;
+    int grid = (int)(want < maxg ? (want > 0 ? want : 1) : maxg);
+    void *args[] = {(void *)&Dt, (void *)&Et, (void *)&bt, (void *)&Dh, (void *)&Ct, (void *)&xt, (void *)&inf,
+                    (void *)&g, (void *)&batch, (void *)&fact, (void *)&solve};
+    e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kWThreads), args, smem, st);
+    if (e != cudaSuccess) return record_cuda_error(e);
+    return BTD_OK;
+}
+
+template <typename T>
+btd_status run_wide(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
+                    void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
+    if (p->n <= 8) return launch_wide<T, 8>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    if (p->n <= 16) return launch_wide<T, 16>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    return launch_wide<T, 32>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+}
+
+template btd_status run_wide<float>(const btd_plan *, int, const void *, const void *, const void *, void *, void *,
+                                    void *, int32_t *, int64_t, int64_t, cudaStream_t);
+template btd_status run_wide<double>(const btd_plan *, int, const void *, const void *, const void *, void *, void *,
+                                     void *, int32_t *, int64_t, int64_t, cudaStream_t);
 
 template btd_status run_persist<float>(const btd_plan *, int, const void *, const void *, const void *, void *, void *,
                                        void *, int32_t *, int64_t, int64_t, cudaStream_t);

@@ -63,6 +63,27 @@ __device__ __forceinline__ double rcp_rn(double x) { return 1.0 / x; }
 __device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
 __device__ __forceinline__ double sqrt_rn(double x) { return sqrt(x); }
 
+// Pivot of a Cholesky step: d = sqrt(a), inv = 1/d. fp32 uses the MUFU reciprocal square root
+// refined by one Newton step (<= 2 ulp, exact for powers of two) instead of the IEEE sqrt and
+// divide sequences, which sit on the POTRF critical path; fp64 keeps the IEEE operations.
+__device__ __forceinline__ void pivot(float a, float &d, float &inv) {
+    float r = rsqrtf(a);
+    r = r * fmaf(-0.5f * a * r, r, 1.5f);
+    inv = r;
+    d = a * r;
+}
+__device__ __forceinline__ void pivot(double a, double &d, double &inv) {
+    d = sqrt(a);
+    inv = 1.0 / d;
+}
+// Reciprocal: fp32 MUFU approximation + one Newton step; fp64 IEEE divide.
+__device__ __forceinline__ float rcp_fast(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * fmaf(-x, r, 2.0f);
+}
+__device__ __forceinline__ double rcp_fast(double x) { return 1.0 / x; }
+
 // v[0..NB) <- p[0..NB), p 16-byte aligned (shared or global).
 template <typename T, int NB>
 __device__ __forceinline__ void vload(T (&v)[NB], const T *p) {
@@ -257,8 +278,8 @@ __device__ __forceinline__ int team_potrf(T (&a)[RPL][NB], T (&dinv)[RPL], const
     for (int k = 0; k < NB; ++k) {
         const T akk = __shfl_sync(kFull, a[k / TS][k], ln.base + k % TS);
         bad = (!(akk > T(0)) && bad < 0) ? k : bad;
-        const T d = sqrt_rn(akk);
-        const T inv = rcp_rn(d);
+        T d, inv;
+        pivot(akk, d, inv);
 #pragma unroll
         for (int t = 0; t < RPL; ++t) {
             const int i = ln.row(t);

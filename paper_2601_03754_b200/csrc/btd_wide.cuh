@@ -1,0 +1,346 @@
+// btd_wide.cuh -- WIDE variant: single long systems (BASELINE configs c2, c3), n <= 32.
+//
+// One cooperative launch; level l of Algorithm 4 (deferred form) is one
+// grid-wide phase in which every column op is executed by a whole CTA (256 threads), and levels
+// are separated by grid.sync(). Compared with one warp per column op (LEVEL / PERSIST-TEAM) this
+// shortens the per-level critical path -- the quantity that sets single-system latency once the
+// first levels no longer fill the GPU -- to: one round of loads, the deferred
+// downdate GEMM, one warp's POTRF, one TRSM per vector (64 vectors in parallel), the downdate and
+// fill GEMMs spread over the CTA. All loops are rolled (n is a runtime value): the kernel's code
+// stays resident in the instruction cache, which the single-warp unrolled variants thrash.
+//
+// Per column c of level l (stride s), with every block staged in shared memory (ld n+1):
+//   l.7   A   = D~_c   - Cd^T Cd        Cd = E^_{l-1,2c/s}   (stored left coupling of column c+s/2)
+//   l.9   Sep = D~_c+s - Ce^T Ce        Ce = E^_{l-1,2c/s+2} (stored left coupling of column c+3s/2)
+//   l.8   A   = chol(A)                 -> Dhat[c]
+//   l.10  Cr  = Cr A^-T                 -> C[slot(l, c/s)]
+//   l.12  Cl  = A^-1 Cl                 -> C[slot(l, c/s-1)]
+//   l.11  Sep -= Cr Cr^T                -> Dhat[c+s]
+//   l.13  C[slot(l+1,(c-s)/2s)] = -Cr Cl
+//   Alg. 6 forward: y_c -= Cd^T y_{c+s/2}; y_c = A^-1 y_c; y_{c+s} -= Ce^T y_{c+3s/2} + Cr y_c
+// and the backward sweep: x_c = A^-T (y_c - Cr^T x_{c+s} - Cl x_{c-s}) one CTA per column.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "btd_kernels.cuh"
+
+namespace btd {
+
+constexpr int kWThreads = 256;
+
+template <typename T>
+struct WideSmem {
+    static __host__ __device__ size_t elems(int n, int m) {
+        const size_t blk = (size_t)n * (n + 1);
+        return 6 * blk + 6 * (size_t)n * m + 2 * (size_t)n + 32;
+    }
+    static __host__ __device__ size_t bytes(int n, int m) { return elems(n, m) * sizeof(T); }
+};
+
+// Cholesky of the n x n block A (ld lda, lower read) by ONE warp: lane r keeps row r of the
+// trailing matrix in a register window whose slot 0 is always the current column, so the column
+// loop is rolled while the register indices stay compile-time. Writes L (lower; strict upper 0)
+// back to A and 1/L[k][k] to dinv. Returns the first failing pivot (<= 0 or NaN) or -1.
+template <typename T, int NB>
+__device__ int warp_potrf_rot(T *A, int lda, int n, T *dinv) {
+    const int r = threadIdx.x & 31;
+    T a[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) a[j] = (r < n && j < n) ? A[r * lda + j] : T(0);
+    int bad = -1;
+    for (int k = 0; k < n; ++k) {
+        const T akk = __shfl_sync(kFull, a[0], k);
+        bad = (!(akk > T(0)) && bad < 0) ? k : bad;
+        T d, inv;
+        pivot(akk, d, inv);
+        const T a0 = (r == k) ? d : a[0] * inv;  // L[r][k] for r >= k
+        if (r >= k && r < n) A[r * lda + k] = a0;
+        if (r == 0) dinv[k] = inv;
+#pragma unroll
+        for (int jj = 1; jj < NB; ++jj) {
+            const T l = __shfl_sync(kFull, a0, (k + jj) & 31);  // L[k+jj][k]
+            a[jj - 1] = fma(-a0, l, a[jj]);                       // A[r][k+jj], shifted into slot jj-1
+        }
+        a[NB - 1] = T(0);
+    }
+    __syncwarp();
+    for (int q = r; q < n * n; q += 32) {
+        const int i = q / n, j = q % n;
+        if (j > i) A[i * lda + j] = T(0);
+    }
+    return bad;
+}
+
+// One thread: x <- L^{-1} x for a vector of length n <= NB in registers (rotating window),
+// L lower in shared memory (ld lda), dinv the reciprocal diagonal; result written to out[i*ostride].
+template <typename T, int NB>
+__device__ void thread_trsv_lower(T (&x)[NB], const T *L, int lda, const T *dinv, int n, T *out, int ostride) {
+    for (int k = 0; k < n; ++k) {
+        const T xk = x[0] * dinv[k];
+        out[(size_t)k * ostride] = xk;
+#pragma unroll
+        for (int jj = 1; jj < NB; ++jj) {
+            const int row = k + jj;
+            const T l = row < n ? L[row * lda + k] : T(0);
+            x[jj - 1] = fma(-xk, l, x[jj]);
+        }
+        x[NB - 1] = T(0);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void wide_copy_block(T *dst, int ldd, const T *src, int n) {
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x) dst[(q / n) * ldd + (q % n)] = src[q];
+}
+
+template <typename T, int NB>
+__device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int32_t *info, const Geo &g, int l,
+                              long long sys, int j, bool fact, bool solve, T *sm) {
+    const int N = g.N, n = g.n, m = g.m;
+    const int lda = n + 1;
+    const size_t nn = (size_t)n * n, blk = (size_t)n * lda;
+    const int s = 1 << (l - 1);
+    const int c = s * (2 * j + 1);
+    const bool hasL = c > s, hasR = c + s <= N;
+    const bool defC = l > 1 && (c + s / 2 <= N);
+    const bool defS = l > 1 && (c + s + s / 2 <= N);
+    const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
+    T *Dh = Dhat + sys * N * nn;
+    T *Cs = C + sys * (size_t)g.nC * nn;
+    T *xs = x ? x + sys * (size_t)N * n * m : nullptr;
+    T *A = sm, *Cr = A + blk, *Cl = Cr + blk, *Cd = Cl + blk, *Ce = Cd + blk, *Sep = Ce + blk;
+    T *yc = Sep + blk, *ys = yc + (size_t)n * m, *yt = ys + (size_t)n * m, *yu = yt + (size_t)n * m;
+    T *dinv = yu + (size_t)n * m;
+    __shared__ int s_bad;
+    const int tid = threadIdx.x, warp = tid >> 5;
+
+    // ---- one round of loads
+    const long long sR = cslot(g, l, c / s), sL = cslot(g, l, hasL ? c / s - 1 : 1);
+    wide_copy_block(A, lda, Dh + (size_t)(c - 1) * nn, n);
+    if (fact) {
+        if (hasR) wide_copy_block(Cr, lda, l == 1 ? Es + (size_t)(c - 1) * nn : Cs + sR * nn, n);
+        if (hasL) wide_copy_block(Cl, lda, l == 1 ? Es + (size_t)(c - 2) * nn : Cs + sL * nn, n);
+        if (hasR) wide_copy_block(Sep, lda, Dh + (size_t)(c + s - 1) * nn, n);
+    } else {
+        if (hasR) wide_copy_block(Cr, lda, Cs + sR * nn, n);
+    }
+    if (defC) wide_copy_block(Cd, lda, Cs + cslot(g, l - 1, 2 * c / s) * nn, n);
+    if (defS) wide_copy_block(Ce, lda, Cs + cslot(g, l - 1, 2 * c / s + 2) * nn, n);
+    if (solve) {
+        for (int q = tid; q < n * m; q += blockDim.x) {
+            yc[q] = xs[(size_t)(c - 1) * n * m + q];
+            if (defC) ys[q] = xs[(size_t)(c + s / 2 - 1) * n * m + q];
+            if (hasR) yt[q] = xs[(size_t)(c + s - 1) * n * m + q];
+            if (defS) yu[q] = xs[(size_t)(c + s + s / 2 - 1) * n * m + q];
+        }
+    }
+    if (tid == 0) s_bad = -1;
+    __syncthreads();
+    // ---- l.7 / l.9 deferred left downdates (lower triangles) and their forward-sweep analogues
+    if (defC || defS) {
+        const int tri = n * (n + 1) / 2;
+        for (int q = tid; q < 2 * tri; q += blockDim.x) {
+            const bool second = q >= tri;
+            if (second ? !defS : !defC) continue;
+            if (!fact) continue;
+            const int qq = second ? q - tri : q;
+            int i = (int)((sqrtf(8.f * qq + 1.f) - 1.f) * 0.5f);
+            while ((i + 1) * (i + 2) / 2 <= qq) ++i;
+            while (i * (i + 1) / 2 > qq) --i;
+            const int jj = qq - i * (i + 1) / 2;
+            const T *M = second ? Ce : Cd;
+            T acc = T(0);
+            for (int k = 0; k < n; ++k) acc = fma(M[k * lda + i], M[k * lda + jj], acc);
+            T *dst = second ? Sep : A;
+            dst[i * lda + jj] -= acc;
+        }
+        if (solve) {
+            for (int q = tid; q < 2 * n * m; q += blockDim.x) {
+                const bool second = q >= n * m;
+                if (second ? !defS : !defC) continue;
+                const int qq = second ? q - n * m : q, i = qq / m, r = qq % m;
+                const T *M = second ? Ce : Cd;
+                const T *src = second ? yu : ys;
+                T acc = T(0);
+                for (int k = 0; k < n; ++k) acc = fma(M[k * lda + i], src[k * m + r], acc);
+                (second ? yt : yc)[qq] -= acc;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- l.8 POTRF (one warp); other warps idle on the barrier
+    if (fact) {
+        if (warp == 0) {
+            const int bad = warp_potrf_rot<T, NB>(A, lda, n, dinv);
+            if ((tid & 31) == 0) s_bad = bad;
+        }
+        __syncthreads();
+        if (s_bad >= 0 && tid == 0) report_fail(info + sys, c);
+        T *dst = Dh + (size_t)(c - 1) * nn;
+        for (int q = tid; q < n * n; q += blockDim.x) dst[q] = A[(q / n) * lda + (q % n)];
+    } else {
+        for (int i = tid; i < n; i += blockDim.x) dinv[i] = rcp_fast(A[i * lda + i]);
+        __syncthreads();
+    }
+    // ---- l.10 / l.12 TRSMs: thread v < n solves row v of Cr, thread n + v column v of Cl;
+    //      the forward solve of y_c runs on the threads after them
+    if (fact) {
+        if (tid < 2 * n) {
+            const bool right = tid < n;
+            const int v = right ? tid : tid - n;
+            if (right ? hasR : hasL) {
+                T xv[NB];
+#pragma unroll
+                for (int k = 0; k < NB; ++k) xv[k] = k < n ? (right ? Cr[v * lda + k] : Cl[k * lda + v]) : T(0);
+                // in-place: row v of Cr / column v of Cl
+                if (right)
+                    thread_trsv_lower<T, NB>(xv, A, lda, dinv, n, Cr + v * lda, 1);
+                else
+                    thread_trsv_lower<T, NB>(xv, A, lda, dinv, n, Cl + v, lda);
+            }
+        }
+    }
+    if (solve && tid >= 64) {
+        for (int r = tid - 64; r < m; r += blockDim.x - 64) {
+            T yv[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) yv[k] = k < n ? yc[k * m + r] : T(0);
+            thread_trsv_lower<T, NB>(yv, A, lda, dinv, n, yc + r, m);
+        }
+    }
+    __syncthreads();
+    if (fact) {
+        if (hasR) {
+            T *dst = Cs + sR * nn;
+            for (int q = tid; q < n * n; q += blockDim.x) dst[q] = Cr[(q / n) * lda + (q % n)];
+        }
+        if (hasL) {
+            T *dst = Cs + sL * nn;
+            for (int q = tid; q < n * n; q += blockDim.x) dst[q] = Cl[(q / n) * lda + (q % n)];
+        }
+    }
+    if (solve)
+        for (int q = tid; q < n * m; q += blockDim.x) xs[(size_t)(c - 1) * n * m + q] = yc[q];
+    // ---- l.11 right downdate and l.13 fill (and the y push into y_{c+s})
+    if (fact && hasR) {
+        T *F = (hasL && hasR) ? Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn : nullptr;
+        for (int q = tid; q < 2 * n * n; q += blockDim.x) {
+            const bool fill = q >= n * n;
+            const int qq = fill ? q - n * n : q, i = qq / n, jj = qq % n;
+            if (fill) {
+                if (!F) continue;
+                T acc = T(0);
+                for (int k = 0; k < n; ++k) acc = fma(Cr[i * lda + k], Cl[k * lda + jj], acc);
+                F[qq] = -acc;
+            } else {
+                T acc = T(0);
+                for (int k = 0; k < n; ++k) acc = fma(Cr[i * lda + k], Cr[jj * lda + k], acc);
+                Dh[(size_t)(c + s - 1) * nn + qq] = Sep[i * lda + jj] - acc;
+            }
+        }
+    } else if (!fact && defS) {
+        // solve-only: nothing to downdate, y pushes below
+    }
+    if (solve && hasR) {
+        for (int q = tid; q < n * m; q += blockDim.x) {
+            const int i = q / m, r = q % m;
+            T acc = T(0);
+            for (int k = 0; k < n; ++k) acc = fma(Cr[i * lda + k], yc[k * m + r], acc);
+            xs[(size_t)(c + s - 1) * n * m + q] = yt[q] - acc;
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T, int NB>
+__device__ void wide_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int l, long long sys, int j, T *sm) {
+    const int N = g.N, n = g.n, m = g.m;
+    const int lda = n + 1;
+    const size_t nn = (size_t)n * n, blk = (size_t)n * lda;
+    const int s = 1 << (l - 1);
+    const int c = s * (2 * j + 1);
+    const bool hasL = c > s, hasR = c + s <= N;
+    const T *Dh = Dhat + sys * N * nn;
+    const T *Cs = C + sys * (size_t)g.nC * nn;
+    T *xs = x + sys * (size_t)N * n * m;
+    T *A = sm, *Cr = A + blk, *Cl = Cr + blk;
+    T *v = Cl + blk, *xr = v + (size_t)n * m, *xl = xr + (size_t)n * m;
+    T *dinv = xl + (size_t)n * m;
+    const int tid = threadIdx.x;
+    wide_copy_block(A, lda, Dh + (size_t)(c - 1) * nn, n);
+    if (hasR) wide_copy_block(Cr, lda, Cs + cslot(g, l, c / s) * nn, n);
+    if (hasL) wide_copy_block(Cl, lda, Cs + cslot(g, l, c / s - 1) * nn, n);
+    for (int q = tid; q < n * m; q += blockDim.x) {
+        v[q] = xs[(size_t)(c - 1) * n * m + q];
+        if (hasR) xr[q] = xs[(size_t)(c + s - 1) * n * m + q];
+        if (hasL) xl[q] = xs[(size_t)(c - s - 1) * n * m + q];
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) dinv[i] = rcp_fast(A[i * lda + i]);
+    for (int q = tid; q < n * m; q += blockDim.x) {
+        const int i = q / m, r = q % m;
+        T acc = T(0);
+        if (hasR)
+            for (int k = 0; k < n; ++k) acc = fma(Cr[k * lda + i], xr[k * m + r], acc);
+        if (hasL)
+            for (int k = 0; k < n; ++k) acc = fma(Cl[i * lda + k], xl[k * m + r], acc);
+        v[q] -= acc;
+    }
+    __syncthreads();
+    // v <- L^{-T} v: thread r per right-hand side, rotating window over rows from the bottom
+    for (int r = tid; r < m; r += blockDim.x) {
+        T w[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) w[k] = k < n ? v[(n - 1 - k) * m + r] : T(0);  // reversed order
+        for (int k = n - 1; k >= 0; --k) {
+            const T xk = w[0] * dinv[k];
+            xs[(size_t)(c - 1) * n * m + (size_t)k * m + r] = xk;
+#pragma unroll
+            for (int jj = 1; jj < NB; ++jj) {
+                const int i = k - jj;
+                const T lk = i >= 0 ? A[k * lda + i] : T(0);  // L[k][i]
+                w[jj - 1] = fma(-lk, xk, w[jj]);
+            }
+            w[NB - 1] = T(0);
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(kWThreads, 1)
+    btd_wide_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C, T *x,
+                    int32_t *info, Geo g, int batch, int fact, int solve) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    extern __shared__ __align__(16) unsigned char wsm_raw[];
+    T *sm = reinterpret_cast<T *>(wsm_raw);
+    {   // a1: Dhat <- D, x <- b, info <- 0
+        const size_t stride = (size_t)gridDim.x * blockDim.x;
+        const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const size_t nD = (size_t)batch * g.N * g.n * g.n, nb = (size_t)batch * g.N * g.n * g.m;
+        if (fact) {
+            if (D != Dhat)
+                for (size_t q = t0; q < nD; q += stride) Dhat[q] = D[q];
+            for (size_t q = t0; q < (size_t)batch; q += stride) info[q] = 0;
+        }
+        if (solve && bvec != x)
+            for (size_t q = t0; q < nb; q += stride) x[q] = bvec[q];
+        grid.sync();
+    }
+    for (int l = 1; l <= g.L; ++l) {
+        const int ncols = ((g.N >> (l - 1)) + 1) / 2;
+        for (long long task = blockIdx.x; task < (long long)batch * ncols; task += gridDim.x)
+            wide_fwd_task<T, NB>(E, Dhat, C, x, info, g, l, task / ncols, (int)(task % ncols), fact, solve, sm);
+        grid.sync();
+    }
+    if (solve) {
+        for (int l = g.L; l >= 1; --l) {
+            const int ncols = ((g.N >> (l - 1)) + 1) / 2;
+            for (long long task = blockIdx.x; task < (long long)batch * ncols; task += gridDim.x)
+                wide_bwd_task<T, NB>(Dhat, C, x, g, l, task / ncols, (int)(task % ncols), sm);
+            grid.sync();
+        }
+    }
+}
+
+}  // namespace btd

@@ -60,7 +60,7 @@ def _check(prob_cast, Dhat, C, x, info, dtype, systems=None, check_L=True):
 SMALL_N = [1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33]
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 12, 16])
 def test_small_grid(variant, dtype, n):
@@ -70,7 +70,7 @@ def test_small_grid(variant, dtype, n):
             _check(*_run(prob, dtype, variant), dtype)
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 @pytest.mark.parametrize("n", [6, 24, 32])
 def test_larger_blocks_and_padding(variant, n):
     for dtype in (torch.float64, torch.float32):
@@ -84,7 +84,7 @@ def test_larger_blocks_and_padding(variant, n):
             _check(*_run(prob, dtype, variant), dtype)
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 @pytest.mark.parametrize("m", [2, 3, 4])
 def test_multiple_rhs(variant, m):
     for dtype in (torch.float64, torch.float32):
@@ -94,7 +94,7 @@ def test_multiple_rhs(variant, m):
         _check(*_run(prob, dtype, variant), dtype)
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 def test_separate_factor_and_solve(variant):
     for dtype in (torch.float64, torch.float32):
         prob = btdgen.kalman(5, 45, 12, m=2, seed=9)
@@ -114,7 +114,7 @@ def _golden_n4(golden, lift):
     return g, btdgen.Problem(D, E, b, None)
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("lift", [False, True])
 def test_golden_n4_bitwise(golden, variant, dtype, lift):
@@ -136,7 +136,7 @@ def test_golden_n4_bitwise(golden, variant, dtype, lift):
         assert torch.equal(x, torch.ones_like(x))
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 @pytest.mark.parametrize("k", [3, 5, 7])
 def test_closed_form_laplacian(variant, k):
     N, n = 2 ** k - 1, 4
@@ -152,7 +152,7 @@ def test_closed_form_laplacian(variant, k):
         assert torch.allclose(C[1, q], exp, atol=1e-12), (lv, kk)
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 def test_identity_and_zero_coupling(variant):
     dev = _dev()
     N, n = 19, 5
@@ -168,7 +168,7 @@ def test_identity_and_zero_coupling(variant):
     assert torch.allclose(x.cpu(), torch.linalg.solve(D, b), atol=1e-12)
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 def test_lower_triangle_only_is_read(variant):
     prob = btdgen.dd(2, 21, 6, seed=3)
     garbage = prob.D + torch.triu(torch.full_like(prob.D, 1e30), 1)
@@ -178,7 +178,7 @@ def test_lower_triangle_only_is_read(variant):
     assert torch.equal(Dh1, Dh2) and torch.equal(C1, C2) and torch.equal(x1, x2)
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 def test_failure_info(variant):
     dev = _dev()
     prob = btdgen.dd(4, 16, 3, seed=2)
@@ -193,7 +193,7 @@ def test_failure_info(variant):
     assert info2.cpu().tolist() == [6, 3, 0, 16]
 
 
-@pytest.mark.parametrize("variant", ["fused", "level", "persist"])
+@pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 def test_deterministic_and_shard_invariant(variant):
     prob = btdgen.kalman(12, 50, 12, seed=4).cast(torch.float32)
     dev = _dev()
@@ -210,7 +210,7 @@ def test_deterministic_and_shard_invariant(variant):
 def test_variants_agree():
     prob = btdgen.dd(3, 77, 12, seed=8)
     _, Dh1, C1, x1, _ = _run(prob, torch.float64, "fused")
-    for v in ("level", "persist"):
+    for v in ("level", "persist", "wide"):
         _, Dh2, C2, x2, _ = _run(prob, torch.float64, v)
         assert (Dh1 - Dh2).abs().max() < 1e-13 and (C1 - C2).abs().max() < 1e-13 and (x1 - x2).abs().max() < 1e-12
 
