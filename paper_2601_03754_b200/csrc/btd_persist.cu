@@ -101,3 +101,13 @@ template btd_status run_persist<float>(const btd_plan *, int, const void *, cons
 template btd_status run_persist<double>(const btd_plan *, int, const void *, const void *, const void *, void *,
                                         void *, void *, int32_t *, int64_t, int64_t, cudaStream_t);
 }  // namespace btd
+
+#ifdef BTD_TIMING
+extern "C" int btd_debug_timing_wide(unsigned long long *host16, int reset) {
+    if (reset) {
+        unsigned long long z[16] = {0};
+        return (int)cudaMemcpyToSymbol(btd::btd_timing, z, sizeof z);
+    }
+    return (int)cudaMemcpyFromSymbol(host16, btd::btd_timing, 16 * sizeof(unsigned long long));
+}
+#endif

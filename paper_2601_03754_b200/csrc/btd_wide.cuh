@@ -95,7 +95,11 @@ __device__ __forceinline__ void wide_copy_block(T *dst, int ldd, const T *src, i
 
 template <typename T, int NB>
 __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int32_t *info, const Geo &g, int l,
-                              long long sys, int j, bool fact, bool solve, T *sm) {
+                              long long sys, int j, bool fact, bool solve, T *sm
+#ifdef BTD_TIMING
+                              , unsigned long long &btd_t_last
+#endif
+) {
     const int N = g.N, n = g.n, m = g.m;
     const int lda = n + 1;
     const size_t nn = (size_t)n * n, blk = (size_t)n * lda;
@@ -136,6 +140,7 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
     }
     if (tid == 0) s_bad = -1;
     __syncthreads();
+    BTD_STAMP(0);
     // ---- l.7 / l.9 deferred left downdates (lower triangles) and their forward-sweep analogues
     if (defC || defS) {
         const int tri = n * (n + 1) / 2;
@@ -168,6 +173,7 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
         }
         __syncthreads();
     }
+    BTD_STAMP(1);
     // ---- l.8 POTRF (one warp); other warps idle on the barrier
     if (fact) {
         if (warp == 0) {
@@ -175,6 +181,7 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
             if ((tid & 31) == 0) s_bad = bad;
         }
         __syncthreads();
+        BTD_STAMP(2);
         if (s_bad >= 0 && tid == 0) report_fail(info + sys, c);
         T *dst = Dh + (size_t)(c - 1) * nn;
         for (int q = tid; q < n * n; q += blockDim.x) dst[q] = A[(q / n) * lda + (q % n)];
@@ -209,6 +216,7 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
         }
     }
     __syncthreads();
+    BTD_STAMP(3);
     if (fact) {
         if (hasR) {
             T *dst = Cs + sR * nn;
@@ -250,6 +258,7 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
         }
     }
     __syncthreads();
+    BTD_STAMP(4);
 }
 
 template <typename T, int NB>
@@ -312,6 +321,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
     btd_wide_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C, T *x,
                     int32_t *info, Geo g, int batch, int fact, int solve) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    BTD_STAMP_INIT();
     extern __shared__ __align__(16) unsigned char wsm_raw[];
     T *sm = reinterpret_cast<T *>(wsm_raw);
     {   // a1: Dhat <- D, x <- b, info <- 0
@@ -330,15 +340,22 @@ __global__ void __launch_bounds__(kWThreads, 1)
     for (int l = 1; l <= g.L; ++l) {
         const int ncols = ((g.N >> (l - 1)) + 1) / 2;
         for (long long task = blockIdx.x; task < (long long)batch * ncols; task += gridDim.x)
-            wide_fwd_task<T, NB>(E, Dhat, C, x, info, g, l, task / ncols, (int)(task % ncols), fact, solve, sm);
+            wide_fwd_task<T, NB>(E, Dhat, C, x, info, g, l, task / ncols, (int)(task % ncols), fact, solve, sm
+#ifdef BTD_TIMING
+                                 , btd_t_last
+#endif
+            );
         grid.sync();
+        BTD_STAMP(5);
     }
     if (solve) {
         for (int l = g.L; l >= 1; --l) {
             const int ncols = ((g.N >> (l - 1)) + 1) / 2;
             for (long long task = blockIdx.x; task < (long long)batch * ncols; task += gridDim.x)
                 wide_bwd_task<T, NB>(Dhat, C, x, g, l, task / ncols, (int)(task % ncols), sm);
+            BTD_STAMP(6);
             grid.sync();
+            BTD_STAMP(7);
         }
     }
 }
