@@ -73,8 +73,14 @@ __device__ __forceinline__ void pivot(float a, float &d, float &inv) {
     d = a * r;
 }
 __device__ __forceinline__ void pivot(double a, double &d, double &inv) {
-    d = sqrt(a);
-    inv = 1.0 / d;
+    // MUFU double-precision rsqrt seed (~2^-23) + two Newton steps (quadratic: ~2^-46, then
+    // ~full precision); keeps the IEEE sqrt/divide sequences off the POTRF critical path.
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    r = r * fma(-0.5 * a * r, r, 1.5);
+    r = r * fma(-0.5 * a * r, r, 1.5);
+    inv = r;
+    d = a * r;
 }
 // Reciprocal: fp32 MUFU approximation + one Newton step; fp64 IEEE divide.
 __device__ __forceinline__ float rcp_fast(float x) {

@@ -39,10 +39,12 @@ struct WideSmem {
 
 // Cholesky of the n x n block A (ld lda, lower read) by ONE warp: lane r keeps row r of the
 // trailing matrix in a register window whose slot 0 is always the current column, so the column
-// loop is rolled while the register indices stay compile-time. Writes L (lower; strict upper 0)
-// back to A and 1/L[k][k] to dinv. Returns the first failing pivot (<= 0 or NaN) or -1.
+// loop is rolled while the register indices stay compile-time. Column k of L is published in A
+// (shared memory) and read back as broadcasts. The forward substitution of the m right-hand
+// sides y (n x m, shared memory) rides along (Alg. 6 l.4 interlaced with l.8). Writes L (lower;
+// strict upper 0) to A and 1/L[k][k] to dinv. Returns the first failing pivot or -1.
 template <typename T, int NB>
-__device__ int warp_potrf_rot(T *A, int lda, int n, T *dinv) {
+__device__ int warp_potrf_rot(T *A, int lda, int n, T *dinv, T *y, int m) {
     const int r = threadIdx.x & 31;
     T a[NB];
 #pragma unroll
@@ -56,19 +58,41 @@ __device__ int warp_potrf_rot(T *A, int lda, int n, T *dinv) {
         const T a0 = (r == k) ? d : a[0] * inv;  // L[r][k] for r >= k
         if (r >= k && r < n) A[r * lda + k] = a0;
         if (r == 0) dinv[k] = inv;
+        if (y && r == k)
+            for (int q = 0; q < m; ++q) y[k * m + q] *= inv;
+        __syncwarp();
 #pragma unroll
         for (int jj = 1; jj < NB; ++jj) {
-            const T l = __shfl_sync(kFull, a0, (k + jj) & 31);  // L[k+jj][k]
-            a[jj - 1] = fma(-a0, l, a[jj]);                       // A[r][k+jj], shifted into slot jj-1
+            const int row = k + jj;
+            const T l = row < n ? A[row * lda + k] : T(0);  // L[k+jj][k], broadcast
+            a[jj - 1] = fma(-a0, l, a[jj]);                 // A[r][k+jj], shifted into slot jj-1
         }
         a[NB - 1] = T(0);
+        if (y && r > k && r < n)
+            for (int q = 0; q < m; ++q) y[r * m + q] = fma(-a0, y[k * m + q], y[r * m + q]);
+        __syncwarp();
     }
-    __syncwarp();
     for (int q = r; q < n * n; q += 32) {
         const int i = q / n, j = q % n;
         if (j > i) A[i * lda + j] = T(0);
     }
     return bad;
+}
+
+// Quad of lanes (4 consecutive) solves L x = b for one vector stored in shared memory with stride
+// xs (x[i*xs]); left-looking, the dot products split over the quad and reduced by shuffles.
+template <typename T>
+__device__ void quad_trsv_lower(const T *L, int lda, const T *dinv, int n, T *x, int xs, bool active) {
+    const int q = threadIdx.x & 3;
+    for (int i = 0; i < n; ++i) {
+        T acc = T(0);
+        if (active)
+            for (int k = q; k < i; k += 4) acc = fma(L[i * lda + k], x[k * xs], acc);
+        acc += __shfl_xor_sync(kFull, acc, 1);
+        acc += __shfl_xor_sync(kFull, acc, 2);
+        if (active && q == 0) x[i * xs] = (x[i * xs] - acc) * dinv[i];
+        __syncwarp();
+    }
 }
 
 // One thread: x <- L^{-1} x for a vector of length n <= NB in registers (rotating window),
@@ -88,9 +112,12 @@ __device__ void thread_trsv_lower(T (&x)[NB], const T *L, int lda, const T *dinv
     }
 }
 
+// Asynchronous (LDGSTS) copy of an n x n global block into shared memory with leading dim ldd;
+// completion: __pipeline_commit() + __pipeline_wait_prior(0) + __syncthreads() by the caller.
 template <typename T>
 __device__ __forceinline__ void wide_copy_block(T *dst, int ldd, const T *src, int n) {
-    for (int q = threadIdx.x; q < n * n; q += blockDim.x) dst[(q / n) * ldd + (q % n)] = src[q];
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x)
+        __pipeline_memcpy_async(dst + (q / n) * ldd + (q % n), src + q, sizeof(T));
 }
 
 template <typename T, int NB>
@@ -139,6 +166,8 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
         }
     }
     if (tid == 0) s_bad = -1;
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
     __syncthreads();
     BTD_STAMP(0);
     // ---- l.7 / l.9 deferred left downdates (lower triangles) and their forward-sweep analogues
@@ -149,10 +178,13 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
             if (second ? !defS : !defC) continue;
             if (!fact) continue;
             const int qq = second ? q - tri : q;
-            int i = (int)((sqrtf(8.f * qq + 1.f) - 1.f) * 0.5f);
-            while ((i + 1) * (i + 2) / 2 <= qq) ++i;
-            while (i * (i + 1) / 2 > qq) --i;
-            const int jj = qq - i * (i + 1) / 2;
+            // qq -> (i, jj), 0 <= jj <= i < n, by walking rows (n <= 32: at most 32 steps)
+            int i = 0, rem = qq;
+            while (rem > i) {
+                rem -= i + 1;
+                ++i;
+            }
+            const int jj = rem;
             const T *M = second ? Ce : Cd;
             T acc = T(0);
             for (int k = 0; k < n; ++k) acc = fma(M[k * lda + i], M[k * lda + jj], acc);
@@ -177,7 +209,7 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
     // ---- l.8 POTRF (one warp); other warps idle on the barrier
     if (fact) {
         if (warp == 0) {
-            const int bad = warp_potrf_rot<T, NB>(A, lda, n, dinv);
+            const int bad = warp_potrf_rot<T, NB>(A, lda, n, dinv, solve ? yc : nullptr, m);
             if ((tid & 31) == 0) s_bad = bad;
         }
         __syncthreads();
@@ -189,30 +221,23 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
         for (int i = tid; i < n; i += blockDim.x) dinv[i] = rcp_fast(A[i * lda + i]);
         __syncthreads();
     }
-    // ---- l.10 / l.12 TRSMs: thread v < n solves row v of Cr, thread n + v column v of Cl;
-    //      the forward solve of y_c runs on the threads after them
-    if (fact) {
-        if (tid < 2 * n) {
-            const bool right = tid < n;
-            const int v = right ? tid : tid - n;
-            if (right ? hasR : hasL) {
-                T xv[NB];
-#pragma unroll
-                for (int k = 0; k < NB; ++k) xv[k] = k < n ? (right ? Cr[v * lda + k] : Cl[k * lda + v]) : T(0);
-                // in-place: row v of Cr / column v of Cl
-                if (right)
-                    thread_trsv_lower<T, NB>(xv, A, lda, dinv, n, Cr + v * lda, 1);
-                else
-                    thread_trsv_lower<T, NB>(xv, A, lda, dinv, n, Cl + v, lda);
+    // ---- l.10 / l.12 TRSMs: quad v (lanes 4v..4v+3) solves row v of Cr (v < n) or column v - n of Cl
+    {
+        const int quad = tid >> 2, qw = quad & 7;  // loops stay warp-uniform (shuffles inside)
+        if (fact) {
+            for (int vb = quad - qw; vb < 2 * n; vb += blockDim.x >> 2) {
+                const int v = vb + qw;
+                const bool right = v < n, inr = v < 2 * n;
+                const int vv = right ? v : (inr ? v - n : 0);
+                const bool active = inr && (right ? hasR : hasL);
+                quad_trsv_lower<T>(A, lda, dinv, n, right ? Cr + vv * lda : Cl + vv, right ? 1 : lda, active);
             }
-        }
-    }
-    if (solve && tid >= 64) {
-        for (int r = tid - 64; r < m; r += blockDim.x - 64) {
-            T yv[NB];
-#pragma unroll
-            for (int k = 0; k < NB; ++k) yv[k] = k < n ? yc[k * m + r] : T(0);
-            thread_trsv_lower<T, NB>(yv, A, lda, dinv, n, yc + r, m);
+        } else if (solve && warp == 0) {
+            // solve-only: y_c <- L^{-1} y_c with the stored factor (one quad per right-hand side)
+            for (int rb = 0; rb < m; rb += 8) {
+                const int r = rb + qw;
+                quad_trsv_lower<T>(A, lda, dinv, n, yc + (r < m ? r : 0), m, r < m);
+            }
         }
     }
     __syncthreads();
@@ -284,6 +309,8 @@ __device__ void wide_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int
         if (hasR) xr[q] = xs[(size_t)(c + s - 1) * n * m + q];
         if (hasL) xl[q] = xs[(size_t)(c - s - 1) * n * m + q];
     }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
     __syncthreads();
     for (int i = tid; i < n; i += blockDim.x) dinv[i] = rcp_fast(A[i * lda + i]);
     for (int q = tid; q < n * m; q += blockDim.x) {
