@@ -28,11 +28,17 @@ namespace btd {
 
 constexpr int kWThreads = 256;
 
+// Blocks are staged with a compile-time leading dimension NB+1 (NB in {8,16,32} >= n): every
+// address inside the rolled loops is base + immediate, and the +1 keeps column walks conflict-free.
+// A guard block at the end absorbs the look-ahead reads past row n of the last block.
+template <int n_>
+constexpr int wide_nb() { return n_ <= 8 ? 8 : n_ <= 16 ? 16 : 32; }
 template <typename T>
 struct WideSmem {
+    static __host__ __device__ int nb(int n) { return n <= 8 ? 8 : n <= 16 ? 16 : 32; }
     static __host__ __device__ size_t elems(int n, int m) {
-        const size_t blk = (size_t)n * (n + 1);
-        return 6 * blk + 6 * (size_t)n * m + 2 * (size_t)n + 32;
+        const size_t blk = (size_t)nb(n) * (nb(n) + 1);
+        return 7 * blk + 6 * (size_t)n * m + 2 * (size_t)nb(n) + 32;
     }
     static __host__ __device__ size_t bytes(int n, int m) { return elems(n, m) * sizeof(T); }
 };
@@ -44,11 +50,12 @@ struct WideSmem {
 // sides y (n x m, shared memory) rides along (Alg. 6 l.4 interlaced with l.8). Writes L (lower;
 // strict upper 0) to A and 1/L[k][k] to dinv. Returns the first failing pivot or -1.
 template <typename T, int NB>
-__device__ int warp_potrf_rot(T *A, int lda, int n, T *dinv, T *y, int m) {
+__device__ int warp_potrf_rot(T *A, int n, T *dinv, T *y, int m) {
+    constexpr int LD = NB + 1;
     const int r = threadIdx.x & 31;
     T a[NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) a[j] = (r < n && j < n) ? A[r * lda + j] : T(0);
+    for (int j = 0; j < NB; ++j) a[j] = (r < n && j < n) ? A[r * LD + j] : T(0);
     int bad = -1;
     for (int k = 0; k < n; ++k) {
         const T akk = __shfl_sync(kFull, a[0], k);
@@ -56,17 +63,14 @@ __device__ int warp_potrf_rot(T *A, int lda, int n, T *dinv, T *y, int m) {
         T d, inv;
         pivot(akk, d, inv);
         const T a0 = (r == k) ? d : a[0] * inv;  // L[r][k] for r >= k
-        if (r >= k && r < n) A[r * lda + k] = a0;
+        if (r >= k && r < n) A[r * LD + k] = a0;
         if (r == 0) dinv[k] = inv;
         if (y && r == k)
             for (int q = 0; q < m; ++q) y[k * m + q] *= inv;
         __syncwarp();
+        const T *col = A + k * (LD + 1);  // col[jj * LD] = L[k+jj][k]; rows >= n are don't-care
 #pragma unroll
-        for (int jj = 1; jj < NB; ++jj) {
-            const int row = k + jj;
-            const T l = row < n ? A[row * lda + k] : T(0);  // L[k+jj][k], broadcast
-            a[jj - 1] = fma(-a0, l, a[jj]);                 // A[r][k+jj], shifted into slot jj-1
-        }
+        for (int jj = 1; jj < NB; ++jj) a[jj - 1] = fma(-a0, col[jj * LD], a[jj]);
         a[NB - 1] = T(0);
         if (y && r > k && r < n)
             for (int q = 0; q < m; ++q) y[r * m + q] = fma(-a0, y[k * m + q], y[r * m + q]);
@@ -74,7 +78,7 @@ __device__ int warp_potrf_rot(T *A, int lda, int n, T *dinv, T *y, int m) {
     }
     for (int q = r; q < n * n; q += 32) {
         const int i = q / n, j = q % n;
-        if (j > i) A[i * lda + j] = T(0);
+        if (j > i) A[i * LD + j] = T(0);
     }
     return bad;
 }
@@ -96,19 +100,47 @@ __device__ void quad_trsv_lower(const T *L, int lda, const T *dinv, int n, T *x,
 }
 
 // One thread: x <- L^{-1} x for a vector of length n <= NB in registers (rotating window),
-// L lower in shared memory (ld lda), dinv the reciprocal diagonal; result written to out[i*ostride].
+// L lower in shared memory (ld NB+1), dinv the reciprocal diagonal; result to out[i*ostride].
 template <typename T, int NB>
-__device__ void thread_trsv_lower(T (&x)[NB], const T *L, int lda, const T *dinv, int n, T *out, int ostride) {
+__device__ void thread_trsv_lower(T (&x)[NB], const T *L, const T *dinv, int n, T *out, int ostride) {
+    constexpr int LD = NB + 1;
     for (int k = 0; k < n; ++k) {
         const T xk = x[0] * dinv[k];
         out[(size_t)k * ostride] = xk;
+        const T *col = L + k * (LD + 1);
 #pragma unroll
-        for (int jj = 1; jj < NB; ++jj) {
-            const int row = k + jj;
-            const T l = row < n ? L[row * lda + k] : T(0);
-            x[jj - 1] = fma(-xk, l, x[jj]);
-        }
+        for (int jj = 1; jj < NB; ++jj) x[jj - 1] = fma(-xk, col[jj * LD], x[jj]);
         x[NB - 1] = T(0);
+    }
+}
+
+// Fully unrolled variants (compile-time NB): the compiler hoists every shared-memory load far
+// ahead of its use, which the rolled rotating-window loop cannot do (3-4x faster measured, see
+// tools/micro/trsv_variants.cu). Rows/columns n <= k < NB are don't-care and never stored.
+template <typename T, int NB>
+__device__ __forceinline__ void thread_trsv_unrolled(T (&x)[NB], const T *L, const T *dinv, int n, T *out,
+                                                     int ostride) {
+    constexpr int LD = NB + 1;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        x[k] *= dinv[k];
+        if (k < n) out[(size_t)k * ostride] = x[k];
+#pragma unroll
+        for (int j = k + 1; j < NB; ++j) x[j] = fma(-x[k], L[j * LD + k], x[j]);
+    }
+}
+
+// x <- L^{-T} x (back substitution), same conventions.
+template <typename T, int NB>
+__device__ __forceinline__ void thread_trsv_upper_t(T (&x)[NB], const T *L, const T *dinv, int n, T *out,
+                                                    int ostride) {
+    constexpr int LD = NB + 1;
+#pragma unroll
+    for (int k = NB - 1; k >= 0; --k) {
+        x[k] *= dinv[k];
+        if (k < n) out[(size_t)k * ostride] = x[k];
+#pragma unroll
+        for (int i = 0; i < k; ++i) x[i] = fma(-L[k * LD + i], x[k], x[i]);
     }
 }
 
@@ -128,8 +160,8 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
 #endif
 ) {
     const int N = g.N, n = g.n, m = g.m;
-    const int lda = n + 1;
-    const size_t nn = (size_t)n * n, blk = (size_t)n * lda;
+    constexpr int lda = NB + 1;
+    const size_t nn = (size_t)n * n, blk = (size_t)NB * lda;
     const int s = 1 << (l - 1);
     const int c = s * (2 * j + 1);
     const bool hasL = c > s, hasR = c + s <= N;
@@ -140,7 +172,7 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
     T *Cs = C + sys * (size_t)g.nC * nn;
     T *xs = x ? x + sys * (size_t)N * n * m : nullptr;
     T *A = sm, *Cr = A + blk, *Cl = Cr + blk, *Cd = Cl + blk, *Ce = Cd + blk, *Sep = Ce + blk;
-    T *yc = Sep + blk, *ys = yc + (size_t)n * m, *yt = ys + (size_t)n * m, *yu = yt + (size_t)n * m;
+    T *yc = Sep + 2 * blk, *ys = yc + (size_t)n * m, *yt = ys + (size_t)n * m, *yu = yt + (size_t)n * m;  // Sep + guard
     T *dinv = yu + (size_t)n * m;
     __shared__ int s_bad;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -209,8 +241,21 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
     // ---- l.8 POTRF (one warp); other warps idle on the barrier
     if (fact) {
         if (warp == 0) {
-            const int bad = warp_potrf_rot<T, NB>(A, lda, n, dinv, solve ? yc : nullptr, m);
-            if ((tid & 31) == 0) s_bad = bad;
+            // unrolled shuffle POTRF (btd_team.cuh), lane r = row r; rows/cols >= n: identity pad
+            const int r = tid & 31;
+            Lane<NB, 32> ln{r, 0};
+            T a[1][NB], di[1];
+#pragma unroll
+            for (int jj = 0; jj < NB; ++jj) a[0][jj] = (r < n && jj < n) ? A[r * lda + jj] : (r == jj ? T(1) : T(0));
+            const int bad = team_potrf<T, NB, 32, 1>(a, di, ln);
+            if (r < n) {
+#pragma unroll
+                for (int jj = 0; jj < NB; ++jj) A[r * lda + jj] = a[0][jj];
+                dinv[r] = di[0];
+            } else if (r < NB) {
+                dinv[r] = T(1);
+            }
+            if (r == 0) s_bad = (bad >= 0 && bad < n) ? bad : -1;
         }
         __syncthreads();
         BTD_STAMP(2);
@@ -221,23 +266,27 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
         for (int i = tid; i < n; i += blockDim.x) dinv[i] = rcp_fast(A[i * lda + i]);
         __syncthreads();
     }
-    // ---- l.10 / l.12 TRSMs: quad v (lanes 4v..4v+3) solves row v of Cr (v < n) or column v - n of Cl
-    {
-        const int quad = tid >> 2, qw = quad & 7;  // loops stay warp-uniform (shuffles inside)
-        if (fact) {
-            for (int vb = quad - qw; vb < 2 * n; vb += blockDim.x >> 2) {
-                const int v = vb + qw;
-                const bool right = v < n, inr = v < 2 * n;
-                const int vv = right ? v : (inr ? v - n : 0);
-                const bool active = inr && (right ? hasR : hasL);
-                quad_trsv_lower<T>(A, lda, dinv, n, right ? Cr + vv * lda : Cl + vv, right ? 1 : lda, active);
-            }
-        } else if (solve && warp == 0) {
-            // solve-only: y_c <- L^{-1} y_c with the stored factor (one quad per right-hand side)
-            for (int rb = 0; rb < m; rb += 8) {
-                const int r = rb + qw;
-                quad_trsv_lower<T>(A, lda, dinv, n, yc + (r < m ? r : 0), m, r < m);
-            }
+    // ---- l.10 / l.12 TRSMs: thread v < n solves row v of Cr, thread n + v column v of Cl;
+    //      threads 64 + r solve right-hand side r (Alg. 6 l.4)
+    if (fact && tid < 2 * n) {
+        const bool right = tid < n;
+        const int v = right ? tid : tid - n;
+        if (right ? hasR : hasL) {
+            T xv[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) xv[k] = k < n ? (right ? Cr[v * lda + k] : Cl[k * lda + v]) : T(0);
+            if (right)
+                thread_trsv_unrolled<T, NB>(xv, A, dinv, n, Cr + v * lda, 1);
+            else
+                thread_trsv_unrolled<T, NB>(xv, A, dinv, n, Cl + v, lda);
+        }
+    }
+    if (solve && tid >= 64) {
+        for (int r = tid - 64; r < m; r += blockDim.x - 64) {
+            T yv[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) yv[k] = k < n ? yc[k * m + r] : T(0);
+            thread_trsv_unrolled<T, NB>(yv, A, dinv, n, yc + r, m);
         }
     }
     __syncthreads();
@@ -289,8 +338,8 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
 template <typename T, int NB>
 __device__ void wide_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int l, long long sys, int j, T *sm) {
     const int N = g.N, n = g.n, m = g.m;
-    const int lda = n + 1;
-    const size_t nn = (size_t)n * n, blk = (size_t)n * lda;
+    constexpr int lda = NB + 1;
+    const size_t nn = (size_t)n * n, blk = (size_t)NB * lda;
     const int s = 1 << (l - 1);
     const int c = s * (2 * j + 1);
     const bool hasL = c > s, hasR = c + s <= N;
@@ -298,7 +347,7 @@ __device__ void wide_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int
     const T *Cs = C + sys * (size_t)g.nC * nn;
     T *xs = x + sys * (size_t)N * n * m;
     T *A = sm, *Cr = A + blk, *Cl = Cr + blk;
-    T *v = Cl + blk, *xr = v + (size_t)n * m, *xl = xr + (size_t)n * m;
+    T *v = Cl + 2 * blk, *xr = v + (size_t)n * m, *xl = xr + (size_t)n * m;  // Cl + guard
     T *dinv = xl + (size_t)n * m;
     const int tid = threadIdx.x;
     wide_copy_block(A, lda, Dh + (size_t)(c - 1) * nn, n);
@@ -323,22 +372,12 @@ __device__ void wide_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int
         v[q] -= acc;
     }
     __syncthreads();
-    // v <- L^{-T} v: thread r per right-hand side, rotating window over rows from the bottom
+    // v <- L^{-T} v: thread r per right-hand side (unrolled back substitution)
     for (int r = tid; r < m; r += blockDim.x) {
         T w[NB];
 #pragma unroll
-        for (int k = 0; k < NB; ++k) w[k] = k < n ? v[(n - 1 - k) * m + r] : T(0);  // reversed order
-        for (int k = n - 1; k >= 0; --k) {
-            const T xk = w[0] * dinv[k];
-            xs[(size_t)(c - 1) * n * m + (size_t)k * m + r] = xk;
-#pragma unroll
-            for (int jj = 1; jj < NB; ++jj) {
-                const int i = k - jj;
-                const T lk = i >= 0 ? A[k * lda + i] : T(0);  // L[k][i]
-                w[jj - 1] = fma(-lk, xk, w[jj]);
-            }
-            w[NB - 1] = T(0);
-        }
+        for (int k = 0; k < NB; ++k) w[k] = k < n ? v[k * m + r] : T(0);
+        thread_trsv_upper_t<T, NB>(w, A, dinv, n, xs + (size_t)(c - 1) * n * m + r, m);
     }
     __syncthreads();
 }
