@@ -83,41 +83,65 @@ __device__ bool cta_potrf(T *A, int n, T *dinv, T *colk) {
         __syncthreads();
         if (threadIdx.x == 0) A[k * n + k] = d;
         // trailing update of the lower triangle: A[i][j] -= L[i][k] L[j][k], k < j <= i
-        const int w = n - k - 1;
-        for (int q = threadIdx.x; q < w * w; q += blockDim.x) {
-            const int ii = q / w, jj = q % w;
-            if (jj > ii) continue;
-            const int i = k + 1 + ii, j = k + 1 + jj;
-            A[i * n + j] = fma(-colk[i], colk[j], A[i * n + j]);
+        // rows over warps, columns over lanes (no integer division in the hot loop)
+        {
+            const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+            for (int i = k + 1 + (threadIdx.x >> 5); i < n; i += nw) {
+                const T li = colk[i];
+                for (int j = k + 1 + lane; j <= i; j += 32) A[i * n + j] = fma(-li, colk[j], A[i * n + j]);
+            }
         }
         __syncthreads();
     }
-    for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
-        const int i = q / n, j = q % n;
-        if (j > i) A[q] = T(0);
-    }
+    for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5)
+        for (int j = i + 1 + (threadIdx.x & 31); j < n; j += 32) A[i * n + j] = T(0);
     __syncthreads();
     return s_ok != 0;
 }
 
-// One warp: x <- L^{-1} x (forward) for V vectors held lane-strided in shared memory rows
-// X[v*n + i]; Lt is L^T (column k of L contiguous: Lt[k*ldt + i] = L[i][k]), dinv the reciprocal diag.
+// One warp: x <- L^{-1} x (forward) for nv <= 4 vectors X[v*n + i] (n <= 128) at once. Lane l
+// holds elements i = l + 32 t of every vector in registers; step k broadcasts x_k of each vector
+// from its owner lane and updates the lane's elements i > k with column k of L (Lt[k*ldt + i]).
 template <typename T>
 __device__ void warp_fwd_subst(T *X, int nv, const T *Lt, int ldt, const T *dinv, int n) {
     const int lane = threadIdx.x & 31;
-    for (int v = 0; v < nv; ++v) {
-        T *x = X + (size_t)v * n;
-        for (int k = 0; k < n; ++k) {
-            T xk = T(0);
-            if (lane == (k & 31)) {
-                xk = x[k] * dinv[k];
-                x[k] = xk;
+    T x[4][4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = lane + 32 * t;
+            x[v][t] = (v < nv && i < n) ? X[(size_t)v * n + i] : T(0);
+        }
+    for (int k = 0; k < n; ++k) {
+        const int owner = k & 31, tk = k >> 5;
+        const T dk = dinv[k];
+        T l[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = lane + 32 * t;
+            l[t] = (i > k && i < n) ? Lt[(size_t)k * ldt + i] : T(0);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            T mine = x[v][0];
+#pragma unroll
+            for (int t = 1; t < 4; ++t) mine = (tk == t) ? x[v][t] : mine;
+            const T xk = __shfl_sync(kFull, mine * dk, owner);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const bool own = (lane == owner) && (t == tk);
+                x[v][t] = own ? xk : fma(-xk, l[t], x[v][t]);
             }
-            xk = __shfl_sync(kFull, xk, k & 31);
-            for (int i = k + 1 + ((lane - (k + 1)) & 31); i < n; i += 32) x[i] = fma(-xk, Lt[(size_t)k * ldt + i], x[i]);
-            __syncwarp();
         }
     }
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = lane + 32 * t;
+            if (v < nv && i < n) X[(size_t)v * n + i] = x[v][t];
+        }
 }
 
 // out(i,j) += sum_k opA(i,k) opB(j,k) over a 64 x 64 tile; opA(i,k) = A[i*lda+k] (ta=0) or A[k*lda+i]
@@ -167,6 +191,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     btd_persist_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C,
                        T *x, int32_t *info, Geo g, int batch, int fact, int solve) {
     cg::grid_group grid = cg::this_grid();
+    BTD_STAMP_INIT();
     {   // phase 0 (a1): Dhat <- D, x <- b, info <- 0
         const size_t stride = (size_t)gridDim.x * blockDim.x;
         const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -223,13 +248,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     cta_copy_in(chunk, Cd + (size_t)k0 * n, (size_t)kc * n);
                     __syncthreads();
                     if (fact) {
-                        for (int q = tid; q < n * n; q += blockDim.x) {
-                            const int i = q / n, jj = q % n;
-                            if (jj > i) continue;
-                            T acc = T(0);
-                            for (int kk = 0; kk < kc; ++kk) acc = fma(chunk[kk * n + i], chunk[kk * n + jj], acc);
-                            A[q] -= acc;
-                        }
+                        for (int i = warp; i < n; i += kPWarps)
+                            for (int jj = (tid & 31); jj <= i; jj += 32) {
+                                T acc = T(0);
+                                for (int kk = 0; kk < kc; ++kk)
+                                    acc = fma(chunk[kk * n + i], chunk[kk * n + jj], acc);
+                                A[i * n + jj] -= acc;
+                            }
                     }
                     if (solve) {  // y_c -= Cd^T y_{c+s/2}
                         for (int q = tid; q < n * m; q += blockDim.x) {
@@ -270,7 +295,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
             __syncthreads();
         }
+        BTD_STAMP(0);
         grid.sync();
+        BTD_STAMP(1);
         // ------------------------------------------------ P2: TRSMs (l.10, l.12)
         if (fact) {
             const long long ntask = (long long)batch * ncols * 2 * nrt;
@@ -294,13 +321,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const T *src = (l == 1) ? (E + sy * (size_t)(N - 1) * nn + (size_t)(side == 0 ? c - 1 : c - 2) * nn)
                                         : (Cs(sy) + slot * nn);
                 T *dst = Cs(sy) + slot * nn;
-                for (size_t q = tid; q < nn; q += blockDim.x) {
-                    const int i = (int)(q / n), k = (int)(q % n);
-                    Lt[(size_t)k * ldt + i] = Dc[q];  // Lt[k][i] = L[i][k]
-                }
-                for (int q = tid; q < nv * n; q += blockDim.x) {
-                    const int v = q / n, i = q % n;
-                    X[q] = side == 0 ? src[(size_t)(v0 + v) * n + i] : src[(size_t)i * n + v0 + v];
+                for (int i = warp; i < n; i += kPWarps)  // Lt[k][i] = L[i][k] (lower part only)
+                    for (int k = (tid & 31); k <= i; k += 32) Lt[(size_t)k * ldt + i] = Dc[(size_t)i * n + k];
+                if (side == 0) {
+                    for (int v = warp; v < nv; v += kPWarps)
+                        for (int i = (tid & 31); i < n; i += 32) X[(size_t)v * n + i] = src[(size_t)(v0 + v) * n + i];
+                } else {
+                    for (int i = warp; i < n; i += kPWarps)
+                        for (int v = (tid & 31); v < nv; v += 32) X[(size_t)v * n + i] = src[(size_t)i * n + v0 + v];
                 }
                 __syncthreads();
                 for (int i = tid; i < n; i += blockDim.x) dinv[i] = rcp_rn(Lt[(size_t)i * ldt + i]);
@@ -310,14 +338,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const int a0 = warp * per, a1 = (a0 + per) < nv ? (a0 + per) : nv;
                 if (a0 < a1) warp_fwd_subst(X + (size_t)a0 * n, a1 - a0, Lt, ldt, dinv, n);
                 __syncthreads();
-                for (int q = tid; q < nv * n; q += blockDim.x) {
-                    const int v = q / n, i = q % n;
-                    if (side == 0) dst[(size_t)(v0 + v) * n + i] = X[q];
-                    else dst[(size_t)i * n + v0 + v] = X[q];
+                if (side == 0) {
+                    for (int v = warp; v < nv; v += kPWarps)
+                        for (int i = (tid & 31); i < n; i += 32) dst[(size_t)(v0 + v) * n + i] = X[(size_t)v * n + i];
+                } else {
+                    for (int i = warp; i < n; i += kPWarps)
+                        for (int v = (tid & 31); v < nv; v += 32) dst[(size_t)i * n + v0 + v] = X[(size_t)v * n + i];
                 }
                 __syncthreads();
             }
+            BTD_STAMP(2);
             grid.sync();
+            BTD_STAMP(3);
         }
         // ------------------------------------------------ P3: l.9 + l.11 syrk, l.13 fill, y pushes
         {
@@ -406,7 +438,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
             }
         }
+        BTD_STAMP(4);
         grid.sync();
+        BTD_STAMP(5);
     }
 
     // ------------------------------------------------ backward sweep
@@ -461,7 +495,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 for (int q = tid; q < n * m; q += blockDim.x) dst[q] = v[q];
                 __syncthreads();
             }
+            BTD_STAMP(6);
             grid.sync();
+            BTD_STAMP(7);
         }
     }
 }
@@ -469,7 +505,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
 }  // namespace btd
 
 namespace btd {
-
 // ---------------------------------------------------------------- PERSIST-TEAM (n <= 32)
 //
 // Same dataflow as the LEVEL variant (Alg. 4 deferred form, one column op per team of lanes,

@@ -11,17 +11,20 @@ import paper_2601_03754_b200 as btd  # noqa: E402
 
 N, n = int(sys.argv[1]), int(sys.argv[2])
 dt = torch.float32 if sys.argv[3] == "f32" else torch.float64
+variant = sys.argv[4] if len(sys.argv) > 4 else "wide"
 fn = btd.lib().btd_debug_timing_wide
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 buf = (ctypes.c_ulonglong * 16)()
 p = btdgen.dd(1, N, n, seed=1, device="cuda").cast(dt)
-btd.factor_solve(p.D, p.E, p.b, variant="wide")
+btd.factor_solve(p.D, p.E, p.b, variant=variant)
 torch.cuda.synchronize()
 fn(buf, 1)
-btd.factor_solve(p.D, p.E, p.b, variant="wide")
+btd.factor_solve(p.D, p.E, p.b, variant=variant)
 torch.cuda.synchronize()
 fn(buf, 0)
-names = ["loads", "deferred", "potrf", "trsm", "l11+fill+stores", "gridsync(fwd)", "bwd task", "gridsync(bwd)"]
+names = (["loads", "deferred", "potrf", "trsm", "l11+fill+stores", "gridsync(fwd)", "bwd task", "gridsync(bwd)"]
+         if variant == "wide" else
+         ["P1 tasks", "P1 sync", "P2 tasks", "P2 sync", "P3 tasks", "P3 sync", "bwd tasks", "bwd sync"])
 tot = sum(buf[i] for i in range(8))
 for i, nm in enumerate(names):
     print(f"{nm:18s} {buf[i]:10d} cycles {buf[i] / max(tot, 1) * 100:5.1f}%")
