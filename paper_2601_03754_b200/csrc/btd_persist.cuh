@@ -22,6 +22,7 @@
 // c3/c4 is 9-85 MB, resident in the 126 MB L2).
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 
 #include "btd_kernels.cuh"
 
@@ -40,7 +41,7 @@ struct PersistSmem {
     // max over phases of the dynamic shared memory (elements)
     static __host__ __device__ size_t elems(int n, int m) {
         const size_t nn = (size_t)n * n;
-        const size_t p1 = nn + (size_t)kPKC * n + 2 * (size_t)n * m + 2 * n;
+        const size_t p1 = nn + (size_t)kPKC * 128 + 2 * (size_t)n * m + n + 256;
         const size_t p2 = (size_t)n * (n + 1) + (size_t)kPRT * n + n;
         const size_t p3 = 2 * (size_t)kPKC * (kPTile + 1);
         const size_t bw = nn + 3 * (size_t)n * m + n;
@@ -54,9 +55,13 @@ struct PersistSmem {
 
 // ---------------------------------------------------------------- CTA helpers
 
+// Global -> shared copy with every element in flight at once (LDGSTS), complete on return for the
+// calling thread (a __syncthreads() makes it CTA-visible).
 template <typename T>
 __device__ __forceinline__ void cta_copy_in(T *dst, const T *src, size_t cnt) {
-    for (size_t q = threadIdx.x; q < cnt; q += blockDim.x) dst[q] = src[q];
+    for (size_t q = threadIdx.x; q < cnt; q += blockDim.x) __pipeline_memcpy_async(dst + q, src + q, sizeof(T));
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
 }
 
 // Right-looking Cholesky of the n x n block A (row-major, ld n) in shared memory; only the lower
@@ -97,6 +102,97 @@ __device__ bool cta_potrf(T *A, int n, T *dinv, T *colk) {
         for (int j = i + 1 + (threadIdx.x & 31); j < n; j += 32) A[i * n + j] = T(0);
     __syncthreads();
     return s_ok != 0;
+}
+
+// CTA-wide Cholesky with the block held in registers, 2-D block-cyclic (n <= 128, 256 threads):
+// thread (warp w, lane) owns A[i][j] for i = w + 8r (r < 16), j = lane + 32c (c < 4). Optionally
+// applies the deferred left downdate A -= Cd^T Cd first (Alg. 4 l.7; Cd global, staged through
+// `chunk` kPKC rows at a time). Step k: the owners of column k publish it (double-buffered
+// `colbuf`, 2n), one barrier, every thread forms L[i][k] = a_ik/d for its rows/columns and applies
+// the rank-1 update to its elements right of column k; column k of L goes straight to A (shared
+// memory). Returns true if every pivot was > 0; dinv[k] = 1/L[k][k]; strict upper triangle = 0.
+template <typename T>
+__device__ bool cta_chol_reg(T *A, int n, const T *Cd, T *chunk, T *colbuf, T *dinv) {
+    constexpr int RR = 16, CC = 4, NP = 128;  // padded order: rows/cols >= n are identity
+    __shared__ int s_ok2;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T a[RR][CC];
+#pragma unroll
+    for (int r = 0; r < RR; ++r)
+#pragma unroll
+        for (int c = 0; c < CC; ++c) {
+            const int i = w + 8 * r, j = lane + 32 * c;
+            a[r][c] = (i < n && j < n) ? A[i * n + j] : (i == j ? T(1) : T(0));
+        }
+    if (threadIdx.x == 0) s_ok2 = 1;
+    if (Cd) {
+        for (int k0 = 0; k0 < n; k0 += kPKC) {
+            const int kc = (n - k0) < kPKC ? (n - k0) : kPKC;
+            __syncthreads();
+            for (int kk = threadIdx.x >> 5; kk < kc; kk += blockDim.x >> 5)
+                for (int i = lane; i < NP; i += 32) chunk[kk * NP + i] = i < n ? Cd[(size_t)(k0 + kk) * n + i] : T(0);
+            __syncthreads();
+            for (int kk = 0; kk < kc; ++kk) {
+                T ci[RR], cj[CC];
+#pragma unroll
+                for (int r = 0; r < RR; ++r) ci[r] = chunk[kk * NP + w + 8 * r];
+#pragma unroll
+                for (int c = 0; c < CC; ++c) cj[c] = chunk[kk * NP + lane + 32 * c];
+#pragma unroll
+                for (int r = 0; r < RR; ++r)
+#pragma unroll
+                    for (int c = 0; c < CC; ++c) a[r][c] = fma(-ci[r], cj[c], a[r][c]);
+            }
+        }
+    }
+    for (int k = 0; k < n; ++k) {
+        T *cb = colbuf + (k & 1) * NP;
+        const int c0 = k >> 5;
+        if (lane == (k & 31)) {
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                T v = a[r][0];
+#pragma unroll
+                for (int c = 1; c < CC; ++c) v = (c == c0) ? a[r][c] : v;
+                cb[w + 8 * r] = v;
+            }
+        }
+        __syncthreads();
+        const T akk = cb[k];
+        T d, inv;
+        pivot(akk, d, inv);
+        T li[RR], lj[CC];
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+            const T v = cb[w + 8 * r] * inv;
+            li[r] = (w + 8 * r > k) ? v : T(0);
+        }
+#pragma unroll
+        for (int c = 0; c < CC; ++c) {
+            const T v = cb[lane + 32 * c] * inv;
+            lj[c] = (lane + 32 * c > k) ? v : T(0);
+        }
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+            for (int c = 0; c < CC; ++c) a[r][c] = fma(-li[r], lj[c], a[r][c]);
+        if (lane == (k & 31)) {  // column k of L to shared memory (rows k..n-1)
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                const int i = w + 8 * r;
+                if (i >= k && i < n) A[i * n + k] = (i == k) ? d : li[r];
+            }
+        }
+        if (threadIdx.x == 0) {
+            dinv[k] = inv;
+            if (!(akk > T(0))) s_ok2 = 0;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5)
+        for (int j = i + 1 + lane; j < n; j += 32) A[i * n + j] = T(0);
+    __syncthreads();
+    return s_ok2 != 0;
 }
 
 // One warp: x <- L^{-1} x (forward) for nv <= 4 vectors X[v*n + i] (n <= 128) at once. Lane l
@@ -227,11 +323,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const int c = s * (2 * j + 1);
             const bool defC = l > 1 && (c + s / 2 <= N);
             T *A = sm;                        // n x n
-            T *chunk = A + nn;                // kPKC x n
-            T *yv = chunk + (size_t)kPKC * n; // n x m (y_c)
+            T *chunk = A + nn;                // kPKC x 128
+            T *yv = chunk + (size_t)kPKC * 128;  // n x m (y_c)
             T *ys = yv + (size_t)n * m;       // n x m (y_{c+s/2})
             T *dinv = ys + (size_t)n * m;     // n
-            T *colk = dinv + n;               // n
+            T *colk = dinv + n;               // 2 x 128 (double-buffered column)
             if (fact) cta_copy_in(A, Dh(sy) + (size_t)(c - 1) * nn, nn);
             else cta_copy_in(A, Dh(sy) + (size_t)(c - 1) * nn, nn);
             if (solve) {
@@ -239,36 +335,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 if (defC) cta_copy_in(ys, xs(sy) + (size_t)(c + s / 2 - 1) * n * m, (size_t)n * m);
             }
             __syncthreads();
-            if (defC) {
-                const T *Cd = Cs(sy) + cslot(g, l - 1, 2 * c / s) * nn;
-                // A -= Cd^T Cd (lower triangle), k-chunked through shared memory
+            const T *Cd = defC ? Cs(sy) + cslot(g, l - 1, 2 * c / s) * nn : nullptr;
+            if (defC && solve) {  // y_c -= Cd^T y_{c+s/2}, Cd staged through `chunk`
                 for (int k0 = 0; k0 < n; k0 += kPKC) {
                     const int kc = (n - k0) < kPKC ? (n - k0) : kPKC;
                     __syncthreads();
                     cta_copy_in(chunk, Cd + (size_t)k0 * n, (size_t)kc * n);
                     __syncthreads();
-                    if (fact) {
-                        for (int i = warp; i < n; i += kPWarps)
-                            for (int jj = (tid & 31); jj <= i; jj += 32) {
-                                T acc = T(0);
-                                for (int kk = 0; kk < kc; ++kk)
-                                    acc = fma(chunk[kk * n + i], chunk[kk * n + jj], acc);
-                                A[i * n + jj] -= acc;
-                            }
-                    }
-                    if (solve) {  // y_c -= Cd^T y_{c+s/2}
-                        for (int q = tid; q < n * m; q += blockDim.x) {
-                            const int i = q / m, qq = q % m;
-                            T acc = T(0);
-                            for (int kk = 0; kk < kc; ++kk) acc = fma(chunk[kk * n + i], ys[(k0 + kk) * m + qq], acc);
-                            yv[q] -= acc;
-                        }
+                    for (int q = tid; q < n * m; q += blockDim.x) {
+                        const int i = q / m, qq = q % m;
+                        T acc = T(0);
+                        for (int kk = 0; kk < kc; ++kk) acc = fma(chunk[kk * n + i], ys[(k0 + kk) * m + qq], acc);
+                        yv[q] -= acc;
                     }
                 }
                 __syncthreads();
             }
             if (fact) {
-                const bool ok = cta_potrf(A, n, dinv, colk);
+                // l.7 deferred downdate + l.8 POTRF, block in registers
+                const bool ok = cta_chol_reg(A, n, Cd, chunk, colk, dinv);
                 if (!ok && tid == 0) report_fail(info + sy, c);
                 T *dst = Dh(sy) + (size_t)(c - 1) * nn;
                 for (size_t q = tid; q < nn; q += blockDim.x) dst[q] = A[q];
