@@ -193,9 +193,12 @@ def _latency_sweep(dev) -> dict:
     out = {}
     cases = [("c1_fp64_n2", 2, torch.float64, [8]), ("c2_fp64_n16", 16, torch.float64, [64]),
              ("c3_fp64_n32", 32, torch.float64, [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]),
-             ("c3_fp32_n32", 32, torch.float32, [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])]
+             ("c3_fp32_n32", 32, torch.float32, [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]),
+             ("c4_fp64_n128", 128, torch.float64, [256])]
+    # n-sweep at N = 512, fp64 (the paper's block-size experiment)
+    nsweep = [("nsweep_fp64_N512_n%d" % n, n, torch.float64, [512]) for n in (4, 8, 12, 16, 24, 32, 48, 64, 96)]
     s = torch.cuda.Stream(dev)
-    for name, n, dt, Ns in cases:
+    for name, n, dt, Ns in cases + nsweep:
         res = {}
         for N in Ns:
             p = btdgen.kalman(1, N, n, seed=N, device=dev).cast(dt)
@@ -209,7 +212,7 @@ def _latency_sweep(dev) -> dict:
                 with torch.cuda.graph(g, stream=s):
                     btd.factor_solve(p.D, p.E, p.b, plan=plan, out=outs)
                 ts = []
-                for _ in range(50):
+                for _ in range(50 if n <= 32 else 5):
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(s)
                     g.replay()

@@ -163,6 +163,16 @@ __device__ __forceinline__ void g_load_row1(T (&v)[NB], const T *blk, int n, int
 // v[k] = blk[k][i] (column i).
 template <typename T, int NB>
 __device__ __forceinline__ void g_load_col1(T (&v)[NB], const T *blk, int n, int i, bool on, bool identity_pad) {
+    if (n == NB) {  // unpadded: compile-time strides, no clamps
+        if (on && i < NB) {
+#pragma unroll
+            for (int k = 0; k < NB; ++k) v[k] = blk[k * NB + i];
+        } else {
+#pragma unroll
+            for (int k = 0; k < NB; ++k) v[k] = (identity_pad && k == i) ? T(1) : T(0);
+        }
+        return;
+    }
     const bool ok = on && i < n;
     const int ic = ok ? i : 0;
 #pragma unroll
@@ -189,6 +199,11 @@ __device__ __forceinline__ void g_store_row1(T *blk, const T (&v)[NB], int n, in
 template <typename T, int NB>
 __device__ __forceinline__ void g_store_col1(T *blk, const T (&v)[NB], int n, int i, bool on) {
     if (!(on && i < n)) return;
+    if (n == NB) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) blk[k * NB + i] = v[k];
+        return;
+    }
     const unsigned long long msk = (n >= 64) ? ~0ull : ((1ull << n) - 1);
 #pragma unroll
     for (int k = 0; k < NB; ++k)
