@@ -116,17 +116,19 @@ __device__ void thread_trsv_lower(T (&x)[NB], const T *L, const T *dinv, int n, 
 
 // Fully unrolled variants (compile-time NB): the compiler hoists every shared-memory load far
 // ahead of its use, which the rolled rotating-window loop cannot do (3-4x faster measured, see
-// tools/micro/trsv_variants.cu). Rows/columns n <= k < NB are don't-care and never stored.
+// tools/micro/trsv_variants.cu).
 template <typename T, int NB>
 __device__ __forceinline__ void thread_trsv_unrolled(T (&x)[NB], const T *L, const T *dinv, int n, T *out,
                                                      int ostride) {
     constexpr int LD = NB + 1;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-        x[k] *= dinv[k];
-        if (k < n) out[(size_t)k * ostride] = x[k];
+        if (k < n) {  // padding rows/columns of L and dinv are never read (may hold stale data)
+            x[k] *= dinv[k];
+            out[(size_t)k * ostride] = x[k];
 #pragma unroll
-        for (int j = k + 1; j < NB; ++j) x[j] = fma(-x[k], L[j * LD + k], x[j]);
+            for (int j = k + 1; j < NB; ++j) x[j] = fma(-x[k], L[j * LD + k], x[j]);
+        }
     }
 }
 
@@ -137,10 +139,12 @@ __device__ __forceinline__ void thread_trsv_upper_t(T (&x)[NB], const T *L, cons
     constexpr int LD = NB + 1;
 #pragma unroll
     for (int k = NB - 1; k >= 0; --k) {
-        x[k] *= dinv[k];
-        if (k < n) out[(size_t)k * ostride] = x[k];
+        if (k < n) {  // see thread_trsv_unrolled: padding never read
+            x[k] *= dinv[k];
+            out[(size_t)k * ostride] = x[k];
 #pragma unroll
-        for (int i = 0; i < k; ++i) x[i] = fma(-L[k * LD + i], x[k], x[i]);
+            for (int i = 0; i < k; ++i) x[i] = fma(-L[k * LD + i], x[k], x[i]);
+        }
     }
 }
 
