@@ -56,11 +56,14 @@ def test_plan_matches_oracle_definitions(N):
 
 
 def test_variant_selection():
-    # c5 (n=12, N=128, fp32) fits one SM's shared memory -> fused; c3 (n=32, N=1024) does not
+    # c5 (n=12, N=128, fp32) fits one SM's shared memory -> fused; single long systems with
+    # n <= 32 whose column ops fit 4 CTAs per SM -> wide (c2, c3); n > 32 -> persist (c4)
     assert btd.Plan(128, 12, 8192, 1, torch.float32).variant == "fused"
-    assert btd.Plan(1024, 32, 1, 1, torch.float64).variant == "persist"
+    assert btd.Plan(1024, 32, 1, 1, torch.float64).variant == "wide"
+    assert btd.Plan(4096, 32, 1, 1, torch.float64).variant == "persist"
     assert btd.Plan(256, 128, 1, 1, torch.float64).variant == "persist"
-    assert btd.Plan(64, 16, 1, 1, torch.float64).variant == "fused"
+    assert btd.Plan(64, 16, 1, 1, torch.float64).variant == "wide"
+    assert btd.Plan(8, 16, 1, 1, torch.float64).variant == "fused"
     assert btd.Plan(8, 2, 1, 1, torch.float64).launches() == 1
     assert btd.Plan(1024, 32, 1, 1, torch.float64).launches() == 1
     p = btd.Plan(1024, 32, 1, 1, torch.float64, variant="level")
