@@ -337,7 +337,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
                      "frac": achieved / pk["hbm"], "traffic": trafficpl,
                      "algorithmic_bytes_per_launch": ab["total"] * B, "peak_source": pk["src"],
-                     "kernel": "btd_fused_r_kernel<float,12,4,32,true,true,1>",
+                     "kernel": "btd_fused_r_kernel<float,12,4,32,true,true,1,true>",
                      "kernel_ms_avg": kern_avg_ms},
         "flops_per_system": algorithmic_flops_per_system(),
         "check": {"max_rel_residual_fp64": agg["max_rel_residual"], "failed_systems": agg["failed_systems"]},

@@ -14,7 +14,8 @@ static btd_status launch_fused_mr(const btd_plan *p, const T *D, const T *E, con
     constexpr int NT = R ? FusedRCfg<T, NB>::NT : FusedCfg<T, NB>::NT;
     void (*kern)(const T *, const T *, const T *, T *, T *, T *, int32_t *, Geo, int);
     if constexpr (R)
-        kern = btd_fused_r_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
+        kern = p->n == NB ? btd_fused_r_kernel<T, NB, TS, NT, FACT, SOLVE, MR, true>
+                          : btd_fused_r_kernel<T, NB, TS, NT, FACT, SOLVE, MR, false>;
     else
         kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
     const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
@@ -156,10 +157,10 @@ btd_status run_typed(const btd_plan *p, int op, const void *D, const void *E, co
 #define BTD_CAT(a, b) BTD_CAT2(a, b)
 extern "C" int BTD_CAT(btd_debug_timing_, BTD_T)(unsigned long long *host16, int reset) {
     if (reset) {
-        unsigned long long z[16] = {0};
+        unsigned long long z[32] = {0};
         return (int)cudaMemcpyToSymbol(btd::btd_timing, z, sizeof z);
     }
-    return (int)cudaMemcpyFromSymbol(host16, btd::btd_timing, 16 * sizeof(unsigned long long));
+    return (int)cudaMemcpyFromSymbol(host16, btd::btd_timing, 32 * sizeof(unsigned long long));
 }
 namespace btd {
 #endif

@@ -48,17 +48,37 @@ __device__ __forceinline__ long long cslot(const Geo &g, int l, int k) { return 
 // Optional phase timing (build with -DBTD_TIMING): CTA 0 accumulates clock64() deltas per phase id
 // into btd_timing[] (read back with cudaMemcpyFromSymbol by tools/phase_times.py).
 #ifdef BTD_TIMING
-static __device__ unsigned long long btd_timing[16];
+static __device__ unsigned long long btd_timing[32];
+// fire-and-forget reduction (RED): the stamp adds no load latency to the phase it closes
 #define BTD_STAMP(id)                                                         \
     do {                                                                      \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                            \
             const unsigned long long now_ = clock64();                        \
-            btd_timing[(id)] += now_ - btd_t_last;                            \
-            btd_t_last = now_;                                                \
+            atomicAdd(&btd_timing[(id)], now_ - btd_t_last);                  \
+            btd_t_last = clock64();                                           \
         }                                                                     \
     } while (0)
-#define BTD_STAMP_INIT() unsigned long long btd_t_last = clock64()
+#define BTD_STAMP_INIT() unsigned long long btd_t_last = clock64(), btd_t_sub = btd_t_last
+// sub-phase stamps on their own clock (do not disturb the phase totals)
+#define BTD_SUB_INIT()                                                        \
+    do {                                                                      \
+        if (blockIdx.x == 0 && threadIdx.x == 0) btd_t_sub = clock64();       \
+    } while (0)
+#define BTD_SUB(cond, id)                                                     \
+    do {                                                                      \
+        if ((cond) && blockIdx.x == 0 && threadIdx.x == 0) {                  \
+            const unsigned long long now_ = clock64();                        \
+            atomicAdd(&btd_timing[(id)], now_ - btd_t_sub);                   \
+            btd_t_sub = clock64();                                            \
+        }                                                                     \
+    } while (0)
 #else
+#define BTD_SUB_INIT() \
+    do {               \
+    } while (0)
+#define BTD_SUB(cond, id) \
+    do {                  \
+    } while (0)
 #define BTD_STAMP(id) \
     do {              \
     } while (0)
@@ -186,6 +206,50 @@ __device__ __forceinline__ int team_potrf_full(T (&a)[RPL][NB], T (&Lf)[NB][NB],
     return bad;
 }
 
+// team_potrf_full fused with the column op's two TRSMs (Alg. 4 l.10, l.12) and, with WY, the
+// forward substitution of y_c (Alg. 6 l.4): the lane's rows of C_r, columns of C_l and y are
+// eliminated as extra rows of the factorization, reusing its pivots and column shuffles, so no
+// copy of L is kept. Operation for operation the same arithmetic as team_potrf_full followed by
+// tri_solve_reg(cr), tri_solve_reg(cl) and fwd_full(y) -- bitwise identical results.
+template <typename T, int NB, int TS, int RPL, bool WY>
+__device__ __forceinline__ int team_potrf_trsm(T (&a)[RPL][NB], T (&cr)[RPL][NB], T (&cl)[RPL][NB], T (&y)[NB],
+                                               const Lane<NB, TS> &ln) {
+    int bad = -1;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const T akk = __shfl_sync(kFull, a[k / TS][k], ln.base + k % TS);
+        bad = (!(akk > T(0)) && bad < 0) ? k : bad;
+        T d, inv;
+        pivot(akk, d, inv);
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+            a[t][k] = (ln.row(t) == k) ? d : a[t][k] * inv;
+            cr[t][k] *= inv;
+            cl[t][k] *= inv;
+        }
+        if (WY) y[k] *= inv;
+        // constant trip count (j > k as a compile-time predicate after unrolling): the unroller
+        // must flatten both loops or the register arrays are demoted to local memory
+#pragma unroll
+        for (int j = 1; j < NB; ++j) {
+            if (j <= k) continue;
+            const T ljk = __shfl_sync(kFull, a[j / TS][k], ln.base + j % TS);
+#pragma unroll
+            for (int t = 0; t < RPL; ++t) {
+                a[t][j] = fma(-a[t][k], ljk, a[t][j]);
+                cr[t][j] = fma(-cr[t][k], ljk, cr[t][j]);
+                cl[t][j] = fma(-cl[t][k], ljk, cl[t][j]);
+            }
+            if (WY) y[j] = fma(-y[k], ljk, y[j]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < RPL; ++t)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) a[t][j] = (j > ln.row(t)) ? T(0) : a[t][j];
+    return bad;
+}
+
 // x <- L^{-1} x with L in registers (per-lane vectors).
 template <typename T, int NB, int RPL>
 __device__ __forceinline__ void tri_solve_reg(T (&x)[RPL][NB], const T (&Lf)[NB][NB], const T (&Linv)[NB]) {
@@ -232,7 +296,42 @@ __device__ __forceinline__ void load_L_full(T (&Lf)[NB][NB], T (&Linv)[NB], cons
     }
 }
 
-template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE, int MR>
+// Backward-sweep cache of FUSED-R (factor+solve). The L^ blocks of levels l >= LC are also written
+// to shared-memory slots that are dead by then, so the backward sweep reads the upper levels from
+// shared memory instead of L2/HBM. The slot of an odd block (its level-1 fill) is dead after level 2,
+// the slot of a block = 2 mod 4 (its level-2 fill) after level 3. Cache entry q lives in the slot of
+// block 2q+1 (q < H1) or 4(q-H1)+2; level l's entries are the D^ blocks of its columns
+// j = 0..ncols-1, then its coupling blocks k = 1..N/s-1 (the C layout).
+struct BwdCache {
+    int LC, H1;
+    __device__ static int count(int N, int l) {
+        const int s = 1 << (l - 1);
+        return ((N / s) + 1) / 2 + (N / s) - 1;
+    }
+    __device__ void init(int N, int L) {
+        H1 = (N + 1) / 2;
+        const int H2 = (N + 2) / 4;
+        LC = L + 1;
+        for (int lc = 3; lc <= 4 && lc <= L; ++lc) {
+            int tot = 0;
+            for (int l = lc; l <= L; ++l) tot += count(N, l);
+            if (tot <= H1 + H2 && count(N, lc) <= (lc == 3 ? H1 : H1 + H2)) {
+                LC = lc;
+                break;
+            }
+        }
+    }
+    __device__ int base(int N, int l) const {  // first cache index of level l >= LC
+        int q = 0;
+        for (int l2 = LC; l2 < l; ++l2) q += count(N, l2);
+        return q;
+    }
+    __device__ int slot(int q) const { return q < H1 ? 2 * q : 4 * (q - H1) + 1; }  // 0-based slot
+};
+
+// EX: n == NB at compile time (no padding): the generic padded load/store paths are not
+// compiled, which keeps the kernel's code (and its instruction-cache footprint) small.
+template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE, int MR, bool EX>
 __global__ void __launch_bounds__(NT *TS, 2)
     btd_fused_r_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C,
                        T *x, int32_t *info, Geo g, int sys0) {
@@ -243,7 +342,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
     T *slots = reinterpret_cast<T *>(smem_raw);
     __shared__ unsigned s_fail;
 
-    const int N = g.N, n = g.n;
+    const int N = g.N, n = EX ? NB : g.n;
     const int m = MR > 0 ? MR : g.m;
     T *Y = slots + (FACT ? (size_t)N * BLK : 0);
     const long long sys = (long long)blockIdx.x + sys0;
@@ -256,6 +355,9 @@ __global__ void __launch_bounds__(NT *TS, 2)
     Lane<NB, TS> ln{lane % TS, lane - lane % TS};
 
     BTD_STAMP_INIT();
+    BwdCache bc;
+    bc.init(N, g.L);
+    if (!(FACT && SOLVE)) bc.LC = g.L + 1;  // LC > L: no cache (factor-only or solve-only)
     if (tid == 0) s_fail = 0xffffffffu;
     fused_load_inputs<T, NB, FACT, SOLVE>(slots, Y, D ? D + sys * N * nn : nullptr,
                                           SOLVE ? bvec + sys * (size_t)N * n * m : nullptr, N, n, m);
@@ -276,50 +378,65 @@ __global__ void __launch_bounds__(NT *TS, 2)
             T cl[RPL][NB];  // lane's columns of the left coupling (kept for phase Y)
             T SL[RPL][NB];  // lane's rows of C_l^T C_l (left downdate, applied in phase Y)
             if (wact) {
-                T Lf[NB][NB], Linv[NB];
+                // FY: factor + single right-hand side -- the TRSMs and y_c's forward substitution
+                // ride along the POTRF (team_potrf_trsm) and no copy of L is kept
+                constexpr bool FY = FACT && SOLVE && MR == 1;
+                T Lf[FY ? 1 : NB][NB], Linv[FY ? 1 : NB];
+                T yv[NB];
                 T cr[RPL][NB];
+                BTD_SUB_INIT();
                 if (FACT) {
-                    // level-1 couplings come from HBM: issue those loads before the POTRF chain
+                    // -- a4 operands: couplings (row q+TS t of the right one, column q+TS t of the
+                    // left one); level 1 reads them from HBM, later levels from the fill slots
                     if (l == 1) {
                         g_load_rows<T, NB, TS, RPL>(cr, Es + (size_t)(c - 1) * nn, n, ln, hasR, false);
                         g_load_cols<T, NB, TS, RPL>(cl, Es + (size_t)((c >= 2 ? c : 2) - 2) * nn, n, ln, hasL, false);
+                    } else {
+                        // a missing coupling (hasR / hasL false) reads some finite block: every use
+                        // of it below is guarded by the same flag
+                        s_load_rows<T, NB, TS, RPL>(cr, slots + (size_t)((hasR ? c + s / 2 : c) - 1) * BLK, ln);
+                        s_load_cols<T, NB, TS, RPL>(cl, slots + (size_t)((hasL ? c - s / 2 : c) - 1) * BLK, ln);
                     }
+                    if (FY) vload<T, NB>(yv, Y + (size_t)(c - 1) * LD);
                     // -- a3: D~_c -> D^_c
                     T a[RPL][NB];
                     s_load_rows<T, NB, TS, RPL>(a, slots + (size_t)(c - 1) * BLK, ln);
                     if (!act) set_identity<T, NB, TS, RPL>(a, ln);
-                    const int bad = team_potrf_full<T, NB, TS, RPL>(a, Lf, Linv, ln);
-                    if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
-                    g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
-                    // -- a4: couplings (row q+TS t of the right one, column q+TS t of the left one)
-                    if (l != 1) {
-                        s_load_rows<T, NB, TS, RPL>(cr, slots + (size_t)((hasR ? c + s / 2 : c) - 1) * BLK, ln);
-                        s_load_cols<T, NB, TS, RPL>(cl, slots + (size_t)((hasL ? c - s / 2 : c) - 1) * BLK, ln);
-#pragma unroll
-                        for (int t = 0; t < RPL; ++t)
-#pragma unroll
-                            for (int q = 0; q < NB; ++q) {
-                                cr[t][q] = hasR ? cr[t][q] : T(0);
-                                cl[t][q] = hasL ? cl[t][q] : T(0);
-                            }
+                    int bad;
+                    if constexpr (FY) {
+                        // Alg. 4 l.8, l.10 (C_r <- C_r D^^{-T}), l.12 (C_l <- D^^{-1} C_l); Alg. 6 l.4
+                        bad = team_potrf_trsm<T, NB, TS, RPL, true>(a, cr, cl, yv, ln);
+                    } else {
+                        bad = team_potrf_full<T, NB, TS, RPL>(a, Lf, Linv, ln);
+                        tri_solve_reg<T, NB, RPL>(cr, Lf, Linv);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
+                        tri_solve_reg<T, NB, RPL>(cl, Lf, Linv);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
                     }
-                    tri_solve_reg<T, NB, RPL>(cr, Lf, Linv);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
-                    tri_solve_reg<T, NB, RPL>(cl, Lf, Linv);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
+                    if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
+                    BTD_SUB(l >= 3, 20);
+                    g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
                     g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
                     g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
-                } else {
+                    if (SOLVE && l >= bc.LC && act) {  // backward-sweep cache (see BwdCache)
+                        const int qb = bc.base(N, l);
+                        s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + j) * BLK, a, ln);
+                        if (hasR) s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK, cr, ln);
+                        if (hasL) s_store_cols<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK, cl, ln);
+                    }
+                } else if constexpr (!FY) {
                     load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
                     g_load_rows<T, NB, TS, RPL>(cr, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
                     g_load_cols<T, NB, TS, RPL>(cl, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
                                                 false);
                 }
+                BTD_SUB(l >= 3, 21);
                 // -- a6: y_c <- D^^{-1} y_c (redundantly in every lane of the team), y_{c+s} -= C_r y_c
                 if (SOLVE) {
                     for (int q = 0; q < m; ++q) {
                         T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
-                        T yv[NB];
-                        vload<T, NB>(yv, yc);
-                        fwd_full<T, NB>(yv, Lf, Linv);
+                        if constexpr (!FY) {
+                            vload<T, NB>(yv, yc);
+                            fwd_full<T, NB>(yv, Lf, Linv);
+                        }
                         __syncwarp();
 #pragma unroll
                         for (int t = 0; t < RPL; ++t) {
@@ -333,6 +450,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                         }
                     }
                 }
+                BTD_SUB(l >= 3, 22);
                 if (FACT) {
                     // -- a2 (right): D~_{c+s} -= C_r C_r^T   (rows of C_r exchanged by shuffles)
                     {
@@ -343,8 +461,10 @@ __global__ void __launch_bounds__(NT *TS, 2)
 #pragma unroll
                             for (int k = 0; k < NB; ++k) {
                                 const T v = __shfl_sync(kFull, cr[jj / TS][k], ln.base + jj % TS);  // C_r[jj][k]
+                                // lower triangle only (row q + TS t >= jj needs t >= jj / TS): the
+                                // separator's upper triangle is never read (potrf reads the lower one)
 #pragma unroll
-                                for (int t = 0; t < RPL; ++t) SR[t][jj] = fma(cr[t][k], v, SR[t][jj]);
+                                for (int t = jj / TS; t < RPL; ++t) SR[t][jj] = fma(cr[t][k], v, SR[t][jj]);
                             }
                         if (hasR) {
                             T *p = slots + (size_t)(c + s - 1) * BLK;
@@ -358,6 +478,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                             }
                         }
                     }
+                    BTD_SUB(l >= 3, 23);
                     // -- a5 fill -C_r C_l -> slot[c], and C_l^T C_l for phase Y (columns of C_l shuffled)
                     {
                         T F[RPL][NB];
@@ -371,11 +492,12 @@ __global__ void __launch_bounds__(NT *TS, 2)
 #pragma unroll
                                 for (int t = 0; t < RPL; ++t) {
                                     F[t][bb] = fma(-cr[t][k], v, F[t][bb]);
-                                    SL[t][bb] = fma(cl[t][k], v, SL[t][bb]);
+                                    if (t >= bb / TS) SL[t][bb] = fma(cl[t][k], v, SL[t][bb]);  // lower only
                                 }
                             }
                         if (hasL && hasR) s_store_rows<T, NB, TS, RPL>(slots + (size_t)(c - 1) * BLK, F, ln);
                     }
+                    BTD_SUB(l >= 3, 24);
                 }
             }
             __syncthreads();
@@ -421,23 +543,38 @@ __global__ void __launch_bounds__(NT *TS, 2)
                 const bool hasL = act && c > s;
                 const bool hasR = act && (c + s <= N);
                 T Lf[NB][NB], Linv[NB];
-                load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
                 T crc[RPL][NB], clr[RPL][NB];
-                g_load_cols<T, NB, TS, RPL>(crc, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
-                g_load_rows<T, NB, TS, RPL>(clr, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
-                                            false);
+                if (l >= bc.LC) {  // upper levels: L^ from the shared-memory cache
+                    const int qb = bc.base(N, l);
+                    const T *pd = slots + (size_t)bc.slot(qb + (act ? j : 0)) * BLK;
+#pragma unroll
+                    for (int i = 0; i < NB; ++i) {
+                        T row[NB];
+                        vload<T, NB>(row, pd + i * LD);
+#pragma unroll
+                        for (int k = 0; k < i; ++k) Lf[i][k] = row[k];
+                        Lf[i][i] = row[i];
+                        Linv[i] = rcp_fast(row[i]);
+                    }
+                    s_load_cols<T, NB, TS, RPL>(crc, hasR ? slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK : pd, ln);
+                    s_load_rows<T, NB, TS, RPL>(clr, hasL ? slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK : pd, ln);
+                } else {
+                    load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
+                    g_load_cols<T, NB, TS, RPL>(crc, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
+                    g_load_rows<T, NB, TS, RPL>(clr, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
+                                                false);
+                }
                 for (int q = 0; q < m; ++q) {
                     T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                     const T *xr = Y + ((size_t)((hasR ? c + s : c) - 1) * m + q) * LD;
                     const T *xl = Y + ((size_t)((hasL ? c - s : c) - 1) * m + q) * LD;
                     T v[NB];
-                    vload<T, NB>(v, yc);
                     T mine[RPL];
 #pragma unroll
                     for (int t = 0; t < RPL; ++t) {
                         const T a = dot<T, NB>(crc[t], xr);  // (C_r^T x_{c+s})[i]
                         const T b2 = dot<T, NB>(clr[t], xl);  // (C_l x_{c-s})[i]
-                        mine[t] = select_idx<T, NB>(v, ln.row(t));
+                        mine[t] = yc[ln.row(t)];
                         mine[t] -= hasR ? a : T(0);
                         mine[t] -= hasL ? b2 : T(0);
                     }
@@ -449,17 +586,20 @@ __global__ void __launch_bounds__(NT *TS, 2)
                     vload<T, NB>(v, yc);
                     bwd_full<T, NB>(v, Lf, Linv);
                     __syncwarp();
+                    // x_c is final: write it to Y (read by the lower levels) and straight to HBM
+                    T *xs = x + (sys * (size_t)N + (c - 1)) * n * m + q;
 #pragma unroll
-                    for (int t = 0; t < RPL; ++t)
-                        if (act) yc[ln.row(t)] = select_idx<T, NB>(v, ln.row(t));
+                    for (int t = 0; t < RPL; ++t) {
+                        const T xv = select_idx<T, NB>(v, ln.row(t));
+                        if (act) yc[ln.row(t)] = xv;
+                        if (act && ln.row(t) < n) xs[(size_t)ln.row(t) * m] = xv;
+                    }
                 }
             }
             __syncthreads();
-            BTD_STAMP(3);
+            BTD_STAMP(l >= 3 ? 25 : 24 + l);  // backward: 25 = levels >= 3, 26 = level 2, 27 = level 1
         }
-        fused_store_x<T, NB>(x + sys * (size_t)N * n * m, Y, N, n, m);
-        __syncthreads();
-        BTD_STAMP(4);
+
     }
     if (FACT && tid == 0) info[sys] = (s_fail == 0xffffffffu) ? 0 : (int)(s_fail & ((1u << 25) - 1));
 }

@@ -105,9 +105,9 @@ template btd_status run_persist<double>(const btd_plan *, int, const void *, con
 #ifdef BTD_TIMING
 extern "C" int btd_debug_timing_wide(unsigned long long *host16, int reset) {
     if (reset) {
-        unsigned long long z[16] = {0};
+        unsigned long long z[32] = {0};
         return (int)cudaMemcpyToSymbol(btd::btd_timing, z, sizeof z);
     }
-    return (int)cudaMemcpyFromSymbol(host16, btd::btd_timing, 16 * sizeof(unsigned long long));
+    return (int)cudaMemcpyFromSymbol(host16, btd::btd_timing, 32 * sizeof(unsigned long long));
 }
 #endif
