@@ -35,6 +35,9 @@
 
 #include "btd_team.cuh"
 
+#ifndef BTD_FR_MINB
+#define BTD_FR_MINB 2
+#endif
 namespace btd {
 
 struct Geo {
@@ -332,12 +335,13 @@ struct BwdCache {
 // EX: n == NB at compile time (no padding): the generic padded load/store paths are not
 // compiled, which keeps the kernel's code (and its instruction-cache footprint) small.
 template <typename T, int NB, int TS, int NT, bool FACT, bool SOLVE, int MR, bool EX>
-__global__ void __launch_bounds__(NT *TS, 2)
+__global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
     btd_fused_r_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C,
                        T *x, int32_t *info, Geo g, int sys0) {
     constexpr int LD = Dims<T, NB>::LD, BLK = Dims<T, NB>::BLK;
     constexpr int RPL = NB / TS;
     constexpr int TPW = 32 / TS;
+    constexpr int NWARP = NT * TS / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *slots = reinterpret_cast<T *>(smem_raw);
     __shared__ unsigned s_fail;
@@ -368,9 +372,18 @@ __global__ void __launch_bounds__(NT *TS, 2)
         const int s = 1 << (l - 1);
         const int ncols = ((N / s) + 1) / 2;
         const long long offL = g.off[l - 1];
+        // Upper levels (fewer columns than teams): G warps share each column op by role, so the
+        // level's critical path is one POTRF+TRSM sweep (every role) plus the longest role:
+        //   role 0: D^ and C_r stores, forward-solve push, right downdate (l.11)
+        //   role 1: fill GEMM (l.13) + C_l^T C_l and the phase-Y left pushes (l.7/l.9)
+        //   role 2 (G = 4): C_l stores; role 3 idle.   G = 2: role 0 also stores C_l.
+        const int G = (FACT && ncols <= TPW) ? 4 : (FACT && ncols <= 2 * TPW) ? 2 : 1;
+        const int GC = NWARP / G;  // warps per role = column groups
+        const int role = warp / GC;
+        const bool doDR = role == 0, doCl = (G == 4) ? role == 2 : role == 0, doFSL = (G == 1) || role == 1;
         for (int j0 = 0; j0 < ncols; j0 += NT) {
-            const int j = j0 + team;
-            const bool wact = j0 + warp * TPW < ncols;
+            const int j = j0 + (warp % GC) * TPW + team % TPW;
+            const bool wact = j0 + (warp % GC) * TPW < ncols;
             const bool act = j < ncols;
             const int c = act ? s * (2 * j + 1) : s;  // inactive teams shadow a valid column, store nothing
             const bool hasL = act && c > s;
@@ -411,16 +424,20 @@ __global__ void __launch_bounds__(NT *TS, 2)
                         tri_solve_reg<T, NB, RPL>(cr, Lf, Linv);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
                         tri_solve_reg<T, NB, RPL>(cl, Lf, Linv);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
                     }
-                    if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
+                    if (act && doDR && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
                     BTD_SUB(l >= 3, 20);
-                    g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
-                    g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
-                    g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
+                    if (doDR) {
+                        g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
+                        g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
+                    }
+                    if (doCl) g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
                     if (SOLVE && l >= bc.LC && act) {  // backward-sweep cache (see BwdCache)
                         const int qb = bc.base(N, l);
-                        s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + j) * BLK, a, ln);
-                        if (hasR) s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK, cr, ln);
-                        if (hasL) s_store_cols<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK, cl, ln);
+                        if (doDR) {
+                            s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + j) * BLK, a, ln);
+                            if (hasR) s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK, cr, ln);
+                        }
+                        if (doCl && hasL) s_store_cols<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK, cl, ln);
                     }
                 } else if constexpr (!FY) {
                     load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
@@ -430,7 +447,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                 }
                 BTD_SUB(l >= 3, 21);
                 // -- a6: y_c <- D^^{-1} y_c (redundantly in every lane of the team), y_{c+s} -= C_r y_c
-                if (SOLVE) {
+                if (SOLVE && doDR) {
                     for (int q = 0; q < m; ++q) {
                         T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                         if constexpr (!FY) {
@@ -453,7 +470,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                 BTD_SUB(l >= 3, 22);
                 if (FACT) {
                     // -- a2 (right): D~_{c+s} -= C_r C_r^T   (rows of C_r exchanged by shuffles)
-                    {
+                    if (doDR) {
                         T SR[RPL][NB];
                         set_zero<T, NB, RPL>(SR);
 #pragma unroll
@@ -480,7 +497,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
                     }
                     BTD_SUB(l >= 3, 23);
                     // -- a5 fill -C_r C_l -> slot[c], and C_l^T C_l for phase Y (columns of C_l shuffled)
-                    {
+                    if (doFSL) {
                         T F[RPL][NB];
                         set_zero<T, NB, RPL>(F);
                         set_zero<T, NB, RPL>(SL);
@@ -503,7 +520,7 @@ __global__ void __launch_bounds__(NT *TS, 2)
             __syncthreads();
             BTD_STAMP(l < 11 ? 5 + l : 1);
             // ---- phase Y: left pushes (deferred left-looking part of Alg. 4, l.7/l.9)
-            if (wact && hasL) {
+            if (wact && hasL && doFSL) {
                 if (FACT) {
                     T *p = slots + (size_t)(c - s - 1) * BLK;
 #pragma unroll
