@@ -38,6 +38,9 @@
 #ifndef BTD_FR_MINB
 #define BTD_FR_MINB 2
 #endif
+#ifndef BTD_SPLIT
+#define BTD_SPLIT 0
+#endif
 namespace btd {
 
 struct Geo {
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
         //   role 0: D^ and C_r stores, forward-solve push, right downdate (l.11)
         //   role 1: fill GEMM (l.13) + C_l^T C_l and the phase-Y left pushes (l.7/l.9)
         //   role 2 (G = 4): C_l stores; role 3 idle.   G = 2: role 0 also stores C_l.
-        const int G = (FACT && ncols <= TPW) ? 4 : (FACT && ncols <= 2 * TPW) ? 2 : 1;
+        const int G = (BTD_SPLIT && FACT && l >= 3 && ncols <= TPW) ? 4 : (BTD_SPLIT && FACT && l >= 3 && ncols <= 2 * TPW) ? 2 : 1;
         const int GC = NWARP / G;  // warps per role = column groups
         const int role = warp / GC;
         const bool doDR = role == 0, doCl = (G == 4) ? role == 2 : role == 0, doFSL = (G == 1) || role == 1;
@@ -425,6 +428,9 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                         tri_solve_reg<T, NB, RPL>(cl, Lf, Linv);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
                     }
                     if (act && doDR && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
+                    // split roles: every role has read D~_c before role 1 overwrites its slot with
+                    // the fill (all warps are active at a split level; G is CTA-uniform)
+                    if (G > 1) __syncthreads();
                     BTD_SUB(l >= 3, 20);
                     if (doDR) {
                         g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
