@@ -39,7 +39,7 @@
 #define BTD_FR_MINB 2
 #endif
 #ifndef BTD_SPLIT
-#define BTD_SPLIT 0
+#define BTD_SPLIT 0  // measured: 3.41M (split) vs 3.62M systems/s (c5); see DESIGN.md
 #endif
 namespace btd {
 
@@ -96,11 +96,15 @@ static __device__ unsigned long long btd_timing[32];
 // ---------------------------------------------------------------------------- shared pieces
 
 // slots <- D (padded with identity), Y <- b (padded rows), cooperative over the CTA.
+// sp >= 0: only blocks [0, sp) and b are waited for on return (asynchronous copies); the copies of
+// blocks [sp, N) stay in flight in the most recent commit group (caller: __pipeline_wait_prior(0)).
 template <typename T, int NB, bool FACT, bool SOLVE>
-__device__ __forceinline__ void fused_load_inputs(T *slots, T *Y, const T *Ds, const T *bs, int N, int n, int m) {
+__device__ __forceinline__ void fused_load_inputs(T *slots, T *Y, const T *Ds, const T *bs, int N, int n, int m,
+                                                  int sp = -1) {
     constexpr int LD = Dims<T, NB>::LD, BLK = Dims<T, NB>::BLK;
     const int tid = threadIdx.x;
     const size_t nn = (size_t)n * n;
+    size_t rest0 = 0, rest1 = 0;  // 16-byte chunks of D still to copy after b
     if (FACT) {
         if (n == NB && LD == NB) {
             constexpr int W = VecT<T>::W;
@@ -110,8 +114,11 @@ __device__ __forceinline__ void fused_load_inputs(T *slots, T *Y, const T *Ds, c
                 using V = typename VecT<T>::type;
                 const V *src = reinterpret_cast<const V *>(Ds);
                 V *dst = reinterpret_cast<V *>(slots);
-                for (size_t q = tid; q < tot / W; q += blockDim.x) __pipeline_memcpy_async(dst + q, src + q, 16);
+                const size_t cut = (sp >= 0 && sp < N && ((size_t)sp * nn) % W == 0) ? (size_t)sp * nn / W : tot / W;
+                for (size_t q = tid; q < cut; q += blockDim.x) __pipeline_memcpy_async(dst + q, src + q, 16);
                 __pipeline_commit();
+                rest0 = cut;
+                rest1 = tot / W;
             } else {
                 for (size_t q = tid; q < tot; q += blockDim.x) slots[q] = Ds[q];
             }
@@ -141,7 +148,16 @@ __device__ __forceinline__ void fused_load_inputs(T *slots, T *Y, const T *Ds, c
             }
         }
     }
-    __pipeline_wait_prior(0);
+    if (rest0 < rest1) {
+        using V = typename VecT<T>::type;
+        const V *src = reinterpret_cast<const V *>(Ds);
+        V *dst = reinterpret_cast<V *>(slots);
+        for (size_t q = rest0 + tid; q < rest1; q += blockDim.x) __pipeline_memcpy_async(dst + q, src + q, 16);
+        __pipeline_commit();
+        __pipeline_wait_prior(1);
+    } else {
+        __pipeline_wait_prior(0);
+    }
 }
 
 template <typename T, int NB>
@@ -366,8 +382,9 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
     bc.init(N, g.L);
     if (!(FACT && SOLVE)) bc.LC = g.L + 1;  // LC > L: no cache (factor-only or solve-only)
     if (tid == 0) s_fail = 0xffffffffu;
+    // level 1's first round touches blocks < 2 NT only: the rest of D lands while it runs
     fused_load_inputs<T, NB, FACT, SOLVE>(slots, Y, D ? D + sys * N * nn : nullptr,
-                                          SOLVE ? bvec + sys * (size_t)N * n * m : nullptr, N, n, m);
+                                          SOLVE ? bvec + sys * (size_t)N * n * m : nullptr, N, n, m, 2 * NT);
     __syncthreads();
     BTD_STAMP(0);
 
@@ -375,12 +392,15 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
         const int s = 1 << (l - 1);
         const int ncols = ((N / s) + 1) / 2;
         const long long offL = g.off[l - 1];
-        // Upper levels (fewer columns than teams): G warps share each column op by role, so the
-        // level's critical path is one POTRF+TRSM sweep (every role) plus the longest role:
-        //   role 0: D^ and C_r stores, forward-solve push, right downdate (l.11)
+        // Upper levels (fewer columns than teams, backward cache active): G warps share each column
+        // op by role. Role 0 (the lead) runs the POTRF+TRSM sweep and writes D^, C_r, C_l to the
+        // shared-memory cache; after one CTA barrier the other roles read C_r, C_l from there:
+        //   role 0: POTRF+TRSM, D^/C_r (and, G = 2, C_l) stores, forward-solve push, l.11 downdate
         //   role 1: fill GEMM (l.13) + C_l^T C_l and the phase-Y left pushes (l.7/l.9)
-        //   role 2 (G = 4): C_l stores; role 3 idle.   G = 2: role 0 also stores C_l.
-        const int G = (BTD_SPLIT && FACT && l >= 3 && ncols <= TPW) ? 4 : (BTD_SPLIT && FACT && l >= 3 && ncols <= 2 * TPW) ? 2 : 1;
+        //   role 2 (G = 4): C_l stores; role 3 idle.
+        // The level's critical path: one sweep + max(role 0's tail, role 1's GEMMs).
+        const bool splitok = BTD_SPLIT && FACT && SOLVE && l >= bc.LC;
+        const int G = (splitok && ncols <= TPW) ? 4 : (splitok && ncols <= 2 * TPW) ? 2 : 1;
         const int GC = NWARP / G;  // warps per role = column groups
         const int role = warp / GC;
         const bool doDR = role == 0, doCl = (G == 4) ? role == 2 : role == 0, doFSL = (G == 1) || role == 1;
@@ -401,7 +421,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                 T yv[NB];
                 T cr[RPL][NB];
                 BTD_SUB_INIT();
-                if (FACT) {
+                if (FACT && doDR) {
                     // -- a4 operands: couplings (row q+TS t of the right one, column q+TS t of the
                     // left one); level 1 reads them from HBM, later levels from the fill slots
                     if (l == 1) {
@@ -427,25 +447,31 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                         tri_solve_reg<T, NB, RPL>(cr, Lf, Linv);  // Alg. 4 l.10: C_r <- C_r D^^{-T}
                         tri_solve_reg<T, NB, RPL>(cl, Lf, Linv);  // Alg. 4 l.12: C_l <- D^^{-1} C_l
                     }
-                    if (act && doDR && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
-                    // split roles: every role has read D~_c before role 1 overwrites its slot with
-                    // the fill (all warps are active at a split level; G is CTA-uniform)
-                    if (G > 1) __syncthreads();
+                    if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
                     BTD_SUB(l >= 3, 20);
-                    if (doDR) {
-                        g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
-                        g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
-                    }
-                    if (doCl) g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
                     if (SOLVE && l >= bc.LC && act) {  // backward-sweep cache (see BwdCache)
                         const int qb = bc.base(N, l);
-                        if (doDR) {
-                            s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + j) * BLK, a, ln);
-                            if (hasR) s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK, cr, ln);
-                        }
-                        if (doCl && hasL) s_store_cols<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK, cl, ln);
+                        s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + j) * BLK, a, ln);
+                        if (hasR) s_store_rows<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK, cr, ln);
+                        if (hasL) s_store_cols<T, NB, TS, RPL>(slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK, cl, ln);
                     }
-                } else if constexpr (!FY) {
+                    g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
+                    g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
+                    if (doCl) g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
+                }
+                if (FACT && G > 1) {
+                    // the lead has read D~_c (role 1 overwrites its slot with the fill) and written
+                    // D^, C_r, C_l to the cache (all warps are active at a split level; G is uniform)
+                    __syncthreads();
+                    if (!doDR) {
+                        const int qb = bc.base(N, l);
+                        const T *pd = slots + (size_t)bc.slot(qb + (act ? j : 0)) * BLK;
+                        s_load_rows<T, NB, TS, RPL>(cr, hasR ? slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK : pd, ln);
+                        s_load_cols<T, NB, TS, RPL>(cl, hasL ? slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK : pd, ln);
+                        if (doCl) g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
+                    }
+                }
+                if constexpr (!FACT && !FY) {
                     load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
                     g_load_rows<T, NB, TS, RPL>(cr, Cs + (offL + c / s - 1) * nn, n, ln, hasR, false);
                     g_load_cols<T, NB, TS, RPL>(cl, Cs + (offL + (c / s >= 2 ? c / s : 2) - 2) * nn, n, ln, hasL,
@@ -547,6 +573,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                     }
                 }
             }
+            if (l == 1 && j0 == 0) __pipeline_wait_prior(0);  // rest of D (fused_load_inputs)
             __syncthreads();
             BTD_STAMP(2);
         }
