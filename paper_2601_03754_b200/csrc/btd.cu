@@ -4,6 +4,7 @@
 // (PAPER.md:569), slot offsets off(l) = sum_{l'<l} (floor(N/2^(l'-1)) - 1), the compiled block
 // size NB >= n (identity padding), the team width and the kernel variant. No device tables:
 // every index is closed form in (level, column) and passed as kernel arguments.
+#include <vector>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -203,23 +204,71 @@ btd_status btd_factor_solve_host(const btd_plan *p, const void *hD, const void *
     const size_t sD = p->N * nn * w, sE = (p->N - 1) * nn * w, sb = p->N * p->n * p->m * w,
                  sC = (size_t)p->geo.nC * nn * w;
     const int64_t per = (p->batch + chunks - 1) / chunks;
-    for (int64_t s0 = 0; s0 < p->batch; s0 += per) {
-        const int64_t cnt = (p->batch - s0) < per ? (p->batch - s0) : per;
-        cudaError_t e;
-#define CP(dst, src, bytes, kind)                                   \
-    e = cudaMemcpyAsync((dst), (src), (bytes), kind, st);           \
-    if (e != cudaSuccess) return cuda_fail(e);
-        CP((char *)dD + s0 * sD, (const char *)hD + s0 * sD, cnt * sD, cudaMemcpyHostToDevice);
-        if (sE) CP((char *)dE + s0 * sE, (const char *)hE + s0 * sE, cnt * sE, cudaMemcpyHostToDevice);
-        CP((char *)db + s0 * sb, (const char *)hb + s0 * sb, cnt * sb, cudaMemcpyHostToDevice);
-        btd_status rs = run(p, 2, dD, dE, db, dDhat, dC, dx, dinfo, s0, cnt, stream);
-        if (rs != BTD_OK) return rs;
-        CP((char *)hDhat + s0 * sD, (const char *)dDhat + s0 * sD, cnt * sD, cudaMemcpyDeviceToHost);
-        if (sC) CP((char *)hC + s0 * sC, (const char *)dC + s0 * sC, cnt * sC, cudaMemcpyDeviceToHost);
-        CP((char *)hx + s0 * sb, (const char *)dx + s0 * sb, cnt * sb, cudaMemcpyDeviceToHost);
-        CP(hinfo + s0, dinfo + s0, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost);
-#undef CP
+    const int nch = (int)((p->batch + per - 1) / per);
+    // Three-stage pipeline: host->device copies on stream `up`, compute on the caller's stream,
+    // device->host copies on stream `down` (the two copy directions run on separate copy engines),
+    // chained per slice by events; the caller's stream finally waits for `down`, so the call stays
+    // asynchronous and ordered on `stream`. Streams/events are released by the driver once the
+    // queued work completes (cudaStreamDestroy / cudaEventDestroy semantics).
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t fork = nullptr, done = nullptr;
+    std::vector<cudaEvent_t> ev_in(nch, nullptr), ev_out(nch, nullptr);
+    cudaError_t e = cudaSuccess;
+    auto cleanup = [&]() {
+        for (auto &x : ev_in)
+            if (x) cudaEventDestroy(x);
+        for (auto &x : ev_out)
+            if (x) cudaEventDestroy(x);
+        if (fork) cudaEventDestroy(fork);
+        if (done) cudaEventDestroy(done);
+        if (up) cudaStreamDestroy(up);
+        if (down) cudaStreamDestroy(down);
+    };
+#define CK(call)                         \
+    do {                                 \
+        e = (call);                      \
+        if (e != cudaSuccess) {          \
+            cleanup();                   \
+            return cuda_fail(e);         \
+        }                                \
+    } while (0)
+    CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    for (int c = 0; c < nch; ++c) {
+        CK(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
     }
+    CK(cudaEventRecord(fork, st));  // everything queued on `stream` before this call comes first
+    CK(cudaStreamWaitEvent(up, fork, 0));
+    CK(cudaStreamWaitEvent(down, fork, 0));
+    for (int c = 0; c < nch; ++c) {
+        const int64_t s0 = c * per;
+        const int64_t cnt = (p->batch - s0) < per ? (p->batch - s0) : per;
+        CK(cudaMemcpyAsync((char *)dD + s0 * sD, (const char *)hD + s0 * sD, cnt * sD, cudaMemcpyHostToDevice, up));
+        if (sE)
+            CK(cudaMemcpyAsync((char *)dE + s0 * sE, (const char *)hE + s0 * sE, cnt * sE, cudaMemcpyHostToDevice, up));
+        CK(cudaMemcpyAsync((char *)db + s0 * sb, (const char *)hb + s0 * sb, cnt * sb, cudaMemcpyHostToDevice, up));
+        CK(cudaEventRecord(ev_in[c], up));
+        CK(cudaStreamWaitEvent(st, ev_in[c], 0));
+        btd_status rs = run(p, 2, dD, dE, db, dDhat, dC, dx, dinfo, s0, cnt, stream);
+        if (rs != BTD_OK) {
+            cleanup();
+            return rs;
+        }
+        CK(cudaEventRecord(ev_out[c], st));
+        CK(cudaStreamWaitEvent(down, ev_out[c], 0));
+        CK(cudaMemcpyAsync((char *)hDhat + s0 * sD, (const char *)dDhat + s0 * sD, cnt * sD, cudaMemcpyDeviceToHost, down));
+        if (sC)
+            CK(cudaMemcpyAsync((char *)hC + s0 * sC, (const char *)dC + s0 * sC, cnt * sC, cudaMemcpyDeviceToHost, down));
+        CK(cudaMemcpyAsync((char *)hx + s0 * sb, (const char *)dx + s0 * sb, cnt * sb, cudaMemcpyDeviceToHost, down));
+        CK(cudaMemcpyAsync(hinfo + s0, dinfo + s0, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost, down));
+    }
+    CK(cudaEventRecord(done, down));
+    CK(cudaStreamWaitEvent(st, done, 0));
+#undef CK
+    cleanup();
     return BTD_OK;
 }
 

@@ -230,7 +230,7 @@ def test_host_entry_point():
     plan = btd.Plan(33, 12, 6, 1, torch.float32)
     ws = btd.HostWorkspace(plan)
     D, E, b = (t.pin_memory() for t in (prob.D, prob.E, prob.b))
-    for chunks in (1, 4):
+    for chunks in (1, 4, 8):  # 8 > batch: one system per slice
         Dhat, C, x, info = btd.factor_solve_host(D, E, b, ws, chunks=chunks)
         torch.cuda.synchronize()
         _check(prob, Dhat.clone(), C.clone(), x.clone(), info.clone(), torch.float32)
