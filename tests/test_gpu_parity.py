@@ -70,6 +70,16 @@ def test_small_grid(variant, dtype, n):
             _check(*_run(prob, dtype, variant), dtype)
 
 
+@pytest.mark.parametrize("dtype,n", [(torch.float32, 12), (torch.float32, 9), (torch.float64, 8)])
+def test_fused_r_horizons(dtype, n):
+    """FUSED-R at horizons that switch its shared-memory backward cache between levels >= 3,
+    >= 4 and off, split level 1 into 1-4 rounds of 32 column ops and stage D in one or two
+    commit groups (N = 37 .. 255; n = 9 runs the padded instantiation, n = 12 / 8 the exact one)."""
+    for N in (37, 63, 64, 65, 100, 128, 129, 200, 255):
+        prob = btdgen.make("kalman", 2, N, n, m=1, seed=300 + N)
+        _check(*_run(prob, dtype, "fused"), dtype)
+
+
 @pytest.mark.parametrize("variant", ["fused", "level", "persist", "wide"])
 @pytest.mark.parametrize("n", [6, 24, 32])
 def test_larger_blocks_and_padding(variant, n):
