@@ -19,11 +19,14 @@ static btd_status launch_fused_mr(const btd_plan *p, const T *D, const T *E, con
     else
         kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
     const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
-    static size_t attr_bytes = 0;  // per instantiation: opt in to > 48 KB dynamic smem once per size
-    if (smem > 48 * 1024 && smem > attr_bytes) {
+    // opt in to > 48 KB dynamic smem once per size -- per KERNEL: the exact-n (EX) and padded
+    // FUSED-R instantiations are two kernels behind one launcher
+    const int kx = (R && p->n == NB) ? 1 : 0;
+    static size_t attr_bytes[2] = {0, 0};
+    if (smem > 48 * 1024 && smem > attr_bytes[kx]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e);
-        attr_bytes = smem;
+        attr_bytes[kx] = smem;
     }
     for (int64_t s0 = 0; s0 < count; s0 += (1ll << 30)) {
         const int64_t cnt = (count - s0) < (1ll << 30) ? (count - s0) : (1ll << 30);
