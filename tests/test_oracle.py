@@ -363,3 +363,88 @@ def test_kalman_is_spd():
         A = dense.assemble(p.D[j].numpy(), p.E[j].numpy())
         w = np.linalg.eigvalsh(A)
         assert w.min() > 0 and w.max() / w.min() < 1e4
+
+
+# ---------------------------------------------------------------- error measures (oracle/metrics.py)
+# Negative pins: each measure is fed a known error and must return the value computed here by hand
+# from its definition, so a dropped term, a wrong norm or a broadcasting slip
+# fails. The exact factor is the hand-worked N=4 instance (tests/golden/nd_n4_scalar.json):
+# Dhat = [2,2,2,2], C = [1,1,1,-0.5] (slots (1,1),(1,2),(1,3),(2,1)), x = [1,1,1,1].
+
+def _golden_factor(golden):
+    g = golden("nd_n4_scalar.json")
+    Dh = np.array(g["Dhat"], float).reshape(4, 1, 1)
+    C = np.array([s[2] for s in g["C_slots"]], float).reshape(4, 1, 1)
+    return g, Dh, C
+
+
+def test_err_L_exact_on_golden_perturbations(golden):
+    _, Dh, C = _golden_factor(golden)
+    assert metrics.err_L(Dh, C, Dh, C) == 0.0
+    # one perturbed element of D^ (block 3): |0.25| / max|L^_o| = 0.25 / 2
+    Dp = Dh.copy()
+    Dp[2, 0, 0] += 0.25
+    assert metrics.err_L(Dp, C, Dh, C) == 0.125
+    # one perturbed element of the level-2 fill slot C(2,1): -0.5 -> -0.25, again 0.25 / 2
+    Cp = C.copy()
+    Cp[3, 0, 0] = -0.25
+    assert metrics.err_L(Dh, Cp, Dh, C) == 0.125
+    # both at once: the max, not the sum, of the two block-set errors
+    assert metrics.err_L(Dp, Cp, Dh, C) == 0.125
+
+
+def test_err_L_denominator_includes_couplings():
+    """max|L^_o| runs over D^ AND every coupling block: with max|C_o| = 4 > max|D^_o| = 1 an error
+    of 1 in D^ reads 1/4 (a denominator over D^ alone would give 1)."""
+    Dh = np.ones((2, 1, 1))
+    C = np.array([4.0]).reshape(1, 1, 1)
+    Dp = Dh.copy()
+    Dp[1, 0, 0] = 2.0
+    assert metrics.err_L(Dp, C, Dh, C) == 0.25
+    Cp = C + 1.0  # error only in C: 1/4 (a numerator over D^ alone would give 0)
+    assert metrics.err_L(Dh, Cp, Dh, C) == 0.25
+
+
+def test_err_x_exact():
+    xo = np.array([1.0, -4.0, 2.0, 0.5]).reshape(4, 1, 1)
+    assert metrics.err_x(xo, xo) == 0.0
+    assert metrics.err_x(2 * xo, xo) == 1.0                     # scaled x: max|x_o| / max|x_o|
+    xp = xo.copy()
+    xp[1] += -1.0                                               # |dx| = 1 at the largest entry
+    assert metrics.err_x(xp, xo) == 0.25                        # / max|x_o| = 4 (not max|x| = 5)
+    xp = xo.copy()
+    xp[2] += 0.5
+    assert metrics.err_x(xp, xo) == 0.125                       # inf-norm, not 2-norm
+    xm = np.stack([xo[..., 0], 3 * xo[..., 0]], -1)             # m = 2 right-hand sides
+    assert metrics.err_x(xm + np.array([0.0, 6.0]), xm) == 0.5  # 6 / max|x_o| = 6 / 12
+
+
+def test_residual_exact_on_golden(golden):
+    g = golden("nd_n4_scalar.json")
+    D = np.array(g["D"]).reshape(4, 1, 1)
+    E = np.array(g["E"]).reshape(3, 1, 1)
+    b = np.array(g["b"]).reshape(4, 1, 1)
+    x = np.ones((4, 1, 1))
+    assert metrics.residual(D, E, x, b) == 0.0
+    # x off by one in block 3: r = Psi e_3 = column 3 of Psi = [0, E_2, D_3, E_3] = [0, 2, 4, 2]
+    xp = x.copy()
+    xp[2] += 1.0
+    exp = math.sqrt(0 + 4 + 16 + 4) / math.sqrt(6 ** 2 + 10 ** 2 + 8 ** 2 + 7.25 ** 2)
+    assert metrics.residual(D, E, xp, b) == pytest.approx(exp, rel=1e-15)
+    # scaled x: r = Psi (2x) - b = b, so the relative residual is exactly 1
+    assert metrics.residual(D, E, 2 * x, b) == pytest.approx(1.0, rel=1e-15)
+
+
+def test_residual_orientation_and_lower_triangle():
+    """n = 2, N = 2 by hand: E_1 = [[1,2],[0,1]] is block (2,1), block (1,2) is E_1^T; only the lower
+    triangle of D_i is read (garbage above the diagonal must not change the result).
+    Psi = [[4,0,1,0],[0,4,2,1],[1,2,4,0],[0,1,0,4]]; Psi e_1 = [4,0,1,0], Psi e_2 = [0,4,2,1]."""
+    D = np.array([[[4.0, 99.0], [0.0, 4.0]], [[4.0, -7.0], [0.0, 4.0]]])
+    E = np.array([[[1.0, 2.0], [0.0, 1.0]]])
+    e1 = np.array([1.0, 0, 0, 0]).reshape(2, 2, 1)
+    e2 = np.array([0, 1.0, 0, 0]).reshape(2, 2, 1)
+    assert metrics.residual(D, E, e1, np.array([4.0, 0, 1, 0]).reshape(2, 2, 1)) == 0.0
+    assert metrics.residual(D, E, e2, np.array([0, 4.0, 2, 1]).reshape(2, 2, 1)) == 0.0
+    # the transposed coupling would give Psi e_1 = [4,0,1,2]: relative residual 2 / |[4,0,1,2]|
+    bt = np.array([4.0, 0, 1, 2]).reshape(2, 2, 1)
+    assert metrics.residual(D, E, e1, bt) == pytest.approx(2.0 / math.sqrt(21.0), rel=1e-15)
