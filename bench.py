@@ -2,22 +2,26 @@
 """Benchmark: batched factor+solve of SPD block-tridiagonal systems on B200 (BASELINE.json config c5).
 
 One "step" = one pass of the whole hot path (load, Schur downdates, potrf,
-trsm, fill gemm, forward and backward sweeps) over one batch of 8192 independent systems with
-n = 12, N = 128, fp32, m = 1 per GPU (weak scaling: each rank owns its own 8192 systems, no
-collective on the data path). Inputs are seeded synthetic ``kalman`` systems
-(btdgen) generated on the device before timing.
+trsm, fill gemm, forward and backward sweeps) over one batch of independent systems with
+n = 12, N = 128, fp32, m = 1. The batch is 8192 systems IN TOTAL, split into contiguous slices
+[r*B/G, (r+1)*B/G) over G ranks (strong scaling, BASELINE.json configs[4] / SURVEY.md §8(e));
+``--scaling weak`` gives every rank its own 8192 systems instead. No collective on the data path.
+Inputs are seeded synthetic ``kalman`` systems (btdgen) generated on the device before timing.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scaling strong|weak]
+  torchrun --nproc-per-node N bench.py --gpus N ...
 
-Rank 0 prints one JSON line. ``--impl reference`` times the CPU oracle (O1, oracle/seqchol.c)
-on the host cores instead (no reference implementation exists for this paper).
+``--gpus N`` (N > 1) without a torchrun environment re-launches itself under
+``torch.distributed.run`` (one process per GPU, rendezvous on 127.0.0.1). Rank 0 prints one
+JSON line. ``--impl reference`` times the CPU oracle (O1, oracle/seqchol.c) on the host cores
+instead (no reference implementation exists for this paper).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import sys
 import threading
@@ -28,11 +32,15 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-B_PER_GPU, N_BLK, N_SZ, M_RHS = 8192, 128, 12, 1
+B_TOTAL, N_BLK, N_SZ, M_RHS = 8192, 128, 12, 1
 DTYPE = torch.float32
 W_BYTES = 4
-METRIC = "batched factor+solve throughput (fp32, n=12, N=128, 8192 systems per GPU)"
 UNIT = "systems/s"
+
+
+def metric_name(scaling: str) -> str:
+    per = "8192 systems in total" if scaling == "strong" else "8192 systems per GPU"
+    return f"batched factor+solve throughput (fp32, n=12, N=128, {per})"
 
 
 def algorithmic_bytes_per_system(N=N_BLK, n=N_SZ, m=M_RHS, w=W_BYTES) -> dict:
@@ -61,21 +69,29 @@ def algorithmic_flops_per_system(N=N_BLK, n=N_SZ, m=M_RHS) -> float:
 
 
 def _peaks() -> dict:
+    """Roofline denominators. HBM: the measured copy bandwidth (MEASURED_PEAKS.json). FP32/FP64 ALU
+    peaks (no tensor cores on these paths): derived from the unit counts and the max SM clock,
+    148 SMs x 128 FP32 / 64 FP64 FMA lanes x 2 flop."""
+    out = dict(hbm=6650.0, src="fallback (B200_PROFILING.md)", mhz=1965.0)
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
-        return dict(hbm=float(pk["hbm_gbs"]), src="measured (MEASURED_PEAKS.json)")
+        out.update(hbm=float(pk["hbm_gbs"]), src="measured (MEASURED_PEAKS.json)",
+                   mhz=float(pk.get("sm_max_mhz", 1965.0)))
     except Exception:
-        return dict(hbm=6650.0, src="fallback (B200_PROFILING.md)")
+        pass
+    out["fp32_tflops"] = 148 * 128 * 2 * out["mhz"] * 1e6 / 1e12
+    out["fp64_tflops"] = 148 * 64 * 2 * out["mhz"] * 1e6 / 1e12
+    return out
 
 
-def _ncu_traffic() -> float | None:
+def _ncu_traffic(batch: int) -> float | None:
     """Per-launch dram bytes of the dominant kernel from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_fused_c5.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        if d.get("config") == [B_PER_GPU, N_BLK, N_SZ, M_RHS, "fp32"]:
+        if d.get("config") == [batch, N_BLK, N_SZ, M_RHS, "fp32"]:
             return float(d["dram_bytes_per_launch"])
     except Exception:
         pass
@@ -89,11 +105,14 @@ class ClockSampler:
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index: int, period: float = 0.01):
+    def __init__(self, index: int | None, period: float = 0.01):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self._stop = threading.Event()
         self.ok = False
+        self.max_mhz = None
+        if index is None:
+            return
         try:
             import pynvml
 
@@ -103,7 +122,7 @@ class ClockSampler:
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception:
-            self.max_mhz = None
+            pass
 
     def _run(self):
         nv = self._nv
@@ -143,16 +162,35 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_oracle_rate(sample_systems: int, steps: int = 1, threads: int | None = None) -> dict:
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _respawn_under_torchrun(nproc: int):
+    """`python bench.py --gpus N` outside torchrun: re-exec as N ranks (one per GPU) on 127.0.0.1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+# ------------------------------------------------------------------ CPU oracle timing (baseline legs)
+
+def cpu_oracle_rate(sample_systems: int, steps: int = 20, warmup: int = 3, threads: int | None = None) -> dict:
     """O1 (Alg. 1 + block substitution, plain C, fp64 accumulation; fp32 inputs upcast) on the
-    host cores over `sample_systems` systems of the same workload; returns systems/s."""
+    host cores over `sample_systems` systems of the same workload; median over `steps` timed
+    passes after `warmup` untimed ones; returns systems/s."""
     import btdgen
     from oracle import o1
 
     prob = btdgen.kalman(sample_systems, N_BLK, N_SZ, seed=5).cast(DTYPE).f64()
     D, E, b = prob.D.numpy(), prob.E.numpy(), prob.b.numpy()
     threads = threads or os.cpu_count() or 1
-    o1.seq_batch(D[:min(64, sample_systems)], E[:min(64, sample_systems)], b[:min(64, sample_systems)], threads)
+    for _ in range(warmup):
+        o1.seq_batch(D, E, b, threads)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -162,21 +200,24 @@ def cpu_oracle_rate(sample_systems: int, steps: int = 1, threads: int | None = N
     t = statistics.median(times)
     return dict(value=sample_systems / t, unit=UNIT, cores=threads, kind="oracle",
                 sample=f"{sample_systems} kalman systems (n=12, N=128, fp32 inputs upcast to fp64), "
-                       f"O1 sequential block Cholesky + solve, {threads} host threads, median of {steps}",
-                seconds_per_step=t)
+                       f"O1 sequential block Cholesky + solve, {threads} host threads, median of {steps} "
+                       f"after {warmup} warm-up passes",
+                seconds_per_step=t, times=times)
 
 
 def run_reference(args):
+    """The base contract's reference arm for this tier: the CPU oracle O1, as it stands, on the
+    host cores; each step a bounded sample (args.ref_sample systems) of the c5 workload."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
     sample = args.ref_sample
-    r = cpu_oracle_rate(sample, steps=args.steps)
+    r = cpu_oracle_rate(sample, steps=args.steps, warmup=args.warmup)
     v = r["value"]
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds_per_step"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (btdgen kalman, seeded)",
+    line = {"impl": "reference", "metric": metric_name(args.scaling), "value": v, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["seconds_per_step"] * 1e3, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (btdgen kalman, seeded)",
             "config": {"workload": "c5 batched MPC-for-RL: fp32 n=12 N=128 m=1, sampled systems on host",
                        "batch_sample": sample, "N": N_BLK, "n": N_SZ, "m": M_RHS},
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -184,12 +225,64 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _latency_sweep(dev) -> dict:
-    """Single-system factor+solve latency (µs) vs N for n=32 (config c3's sweep), c1 and c2;
-    CUDA-graph replay, warm L2, median of 50."""
+# ------------------------------------------------------------------ single-system latency (§8(d) regime 1)
+
+def _l2_flusher(dev):
+    """A buffer of 2x the L2 size; writing it evicts the system's data from L2."""
+    try:
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    except Exception:
+        l2 = 126 << 20
+    buf = torch.empty(max(2 * l2, 64 << 20) // 4, dtype=torch.float32, device=dev)
+    return lambda: buf.fill_(1.0)
+
+
+def _latency_case(dev, s, N, n, dt, reps, flush):
     import btdgen
     import paper_2601_03754_b200 as btd
 
+    p = btdgen.kalman(1, N, n, seed=N, device=dev).cast(dt)
+    plan = btd.Plan(N, n, 1, 1, dt)
+    outs = (torch.empty_like(p.D), torch.empty(1, plan.num_coupling_blocks, n, n, dtype=dt, device=dev),
+            torch.empty_like(p.b), torch.empty(1, dtype=torch.int32, device=dev))
+
+    def call():
+        btd.factor_solve(p.D, p.E, p.b, plan=plan, out=outs, stream=s)
+
+    def timed(fn, pre=None):
+        ts = []
+        for _ in range(reps):
+            if pre is not None:
+                pre()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        return round(statistics.median(ts), 2)
+
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            call()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            call()
+        r = {"variant": plan.variant,
+             "graph_warm": timed(g.replay),
+             "graph_l2_flushed": timed(g.replay, flush),
+             "host_launch_warm": timed(call)}
+    assert int(outs[3].abs().sum()) == 0
+    return r
+
+
+def _latency_sweep(dev) -> dict:
+    """Single-system factor+solve latency (µs) for c1, c2, the c3 N-sweep (fp32 and fp64), c4 and
+    the n-sweep at N = 512: CUDA-graph replay with warm L2, graph replay after an L2 flush, and
+    host-launched calls (warm); median of 50 (5 for n > 32). Each case also carries its
+    throughput floor max(flops / ALU peak, bytes / HBM peak) and that floor's fraction of the
+    graph-replay time (SURVEY.md §8(d) "Per-regime roofline statement")."""
+    pk = _peaks()
     out = {}
     cases = [("c1_fp64_n2", 2, torch.float64, [8]), ("c2_fp64_n16", 16, torch.float64, [64]),
              ("c3_fp64_n32", 32, torch.float64, [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]),
@@ -198,173 +291,232 @@ def _latency_sweep(dev) -> dict:
     # n-sweep at N = 512, fp64 (the paper's block-size experiment)
     nsweep = [("nsweep_fp64_N512_n%d" % n, n, torch.float64, [512]) for n in (4, 8, 12, 16, 24, 32, 48, 64, 96)]
     s = torch.cuda.Stream(dev)
+    flush = _l2_flusher(dev)
     for name, n, dt, Ns in cases + nsweep:
         res = {}
+        w = 8 if dt == torch.float64 else 4
         for N in Ns:
-            p = btdgen.kalman(1, N, n, seed=N, device=dev).cast(dt)
-            plan = btd.Plan(N, n, 1, 1, dt)
-            outs = (torch.empty_like(p.D), torch.empty(1, plan.num_coupling_blocks, n, n, dtype=dt, device=dev),
-                    torch.empty_like(p.b), torch.empty(1, dtype=torch.int32, device=dev))
-            with torch.cuda.stream(s):
-                for _ in range(3):
-                    btd.factor_solve(p.D, p.E, p.b, plan=plan, out=outs)
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=s):
-                    btd.factor_solve(p.D, p.E, p.b, plan=plan, out=outs)
-                ts = []
-                for _ in range(50 if n <= 32 else 5):
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(s)
-                    g.replay()
-                    e1.record(s)
-                    e1.synchronize()
-                    ts.append(e0.elapsed_time(e1) * 1e3)
-            res[str(N)] = round(statistics.median(ts), 2)
-            res[f"{N}_variant"] = plan.variant
+            r = _latency_case(dev, s, N, n, dt, 50 if n <= 32 else 5, flush)
+            fl = algorithmic_flops_per_system(N, n, 1)
+            by = algorithmic_bytes_per_system(N, n, 1, w)["total"]
+            t_fp = fl / ((pk["fp64_tflops"] if w == 8 else pk["fp32_tflops"]) * 1e12) * 1e6
+            t_hbm = by / (pk["hbm"] * 1e9) * 1e6
+            r["floor_us"] = round(max(t_fp, t_hbm), 3)
+            r["floor_bound"] = "alu" if t_fp >= t_hbm else "hbm"
+            r["floor_frac"] = round(r["floor_us"] / r["graph_warm"], 5)
+            res[str(N)] = r
         out[name] = res
     return out
 
 
-def run_ours(args):
-    import btdgen
+# ------------------------------------------------------------------ the batched benchmark, one rank
+
+class _CudaClock:
+    """Device time with CUDA events on the launching stream."""
+
+    def __init__(self, stream):
+        self.s = stream
+
+    def mark(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self.s)
+        return e
+
+    @staticmethod
+    def ms(a, b) -> float:
+        return a.elapsed_time(b)
+
+    def sync(self):
+        self.s.synchronize()
+
+
+class _HostClock:
+    """Wall time; used only by the CPU (gloo) test of the rank/aggregation path."""
+
+    def mark(self):
+        return time.perf_counter()
+
+    @staticmethod
+    def ms(a, b) -> float:
+        return (b - a) * 1e3
+
+    def sync(self):
+        pass
+
+
+def _gpu_step_factory(prob, dev, stream):
+    """The product path: one btd_factor_solve launch over the rank's batch on `stream`."""
     import paper_2601_03754_b200 as btd
 
-    ws, rank, local = _dist()
-    if args.gpus > 1 or ws > 1:
-        import torch.distributed as dist
+    B = prob.D.shape[0]
+    plan = btd.Plan(N_BLK, N_SZ, B, M_RHS, DTYPE)
+    out = (torch.empty_like(prob.D),
+           torch.empty(B, plan.num_coupling_blocks, N_SZ, N_SZ, dtype=DTYPE, device=dev),
+           torch.empty_like(prob.b), torch.empty(B, dtype=torch.int32, device=dev))
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if ws > 1 else 0)
-    torch.cuda.set_device(dev)
+    def step():
+        btd.factor_solve(prob.D, prob.E, prob.b, plan=plan, out=out, stream=stream)
+
+    return step, out, plan
+
+
+def run_rank(args, rank: int, world: int, dev: torch.device, step_factory=None, barrier=None) -> dict:
+    """One rank of the batched benchmark: shard -> generate its systems from their global indices ->
+    W warm-up steps -> barrier -> K timed steps (device clock on the launching stream) -> barrier
+    -> fp64 residual check of every system -> per-rank statistics (shard.STAT_FIELDS).
+    ``step_factory(prob, dev, stream) -> (step, (Dhat, C, x, info), plan)``; the default is the
+    CUDA path. The CPU gloo test passes a host stub to drive the same shard/gather/aggregate code."""
+    import btdgen
     from paper_2601_03754_b200 import shard
 
-    first, B = shard.shard_range(rank, max(ws, 1), args.batch)
+    first, B = shard.shard_range(rank, world, args.batch, args.scaling)
     prob = btdgen.kalman(B, N_BLK, N_SZ, m=M_RHS, seed=5, first_system=first, device=dev).cast(DTYPE)
-    D, E, b = prob.D, prob.E, prob.b
-    plan = btd.Plan(N_BLK, N_SZ, B, M_RHS, DTYPE)
-    Dhat = torch.empty_like(D)
-    C = torch.empty(B, plan.num_coupling_blocks, N_SZ, N_SZ, dtype=DTYPE, device=dev)
-    x = torch.empty_like(b)
-    info = torch.empty(B, dtype=torch.int32, device=dev)
-    stream = torch.cuda.Stream(dev)
-    out = (Dhat, C, x, info)
+    on_gpu = dev.type == "cuda"
+    stream = torch.cuda.Stream(dev) if on_gpu else None
+    step, out, plan = (step_factory or _gpu_step_factory)(prob, dev, stream)
+    Dhat, C, x, info = out
+    clock = _CudaClock(stream) if on_gpu else _HostClock()
+    barrier = barrier or (lambda: None)
 
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            btd.factor_solve(D, E, b, plan=plan, out=out, stream=stream)
-    stream.synchronize()
+    for _ in range(args.warmup):
+        step()
+    clock.sync()
     assert int(info.abs().sum()) == 0, "factorization failed in warm-up"
 
-    # ---- timed region: K steps, barrier + synchronize on both sides, CUDA events on `stream`
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(dev.index) as clk:
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        with torch.cuda.stream(stream):
-            for k in range(args.steps):
-                ev[k][0].record(stream)
-                btd.factor_solve(D, E, b, plan=plan, out=out, stream=stream)
-                ev[k][1].record(stream)
-        t_end.record(stream)
+    # ---- timed region: K steps, barrier + synchronize on both sides, device events on `stream`
+    barrier()
+    if on_gpu:
         torch.cuda.synchronize(dev)
-    if ws > 1:
-        torch.distributed.barrier()
-    t_total = t_start.elapsed_time(t_end) / 1e3
-    kern_ms = [a.elapsed_time(c) for a, c in ev]
-    launches = args.steps * plan.launches("factor_solve")
+    marks = []
+    with ClockSampler(dev.index if on_gpu else None) as clk:
+        t0 = clock.mark()
+        for _ in range(args.steps):
+            a = clock.mark()
+            step()
+            marks.append((a, clock.mark()))
+        t1 = clock.mark()
+        if on_gpu:
+            torch.cuda.synchronize(dev)
+    barrier()
+    t_total = clock.ms(t0, t1) / 1e3
+    kern_ms = [clock.ms(a, b) for a, b in marks]
 
-    # ---- correctness spot check of the timed outputs (after timing): residual of every system in fp64
-    r = btdgen.block_tridiag_matvec(D.double(), E.double(), x.double()) - b.double()
-    rel = (r.flatten(1).norm(dim=1) / b.double().flatten(1).norm(dim=1)).max().item()
+    # ---- correctness check of the timed outputs (after timing): residual of every system in fp64
+    r = btdgen.block_tridiag_matvec(prob.D.double(), prob.E.double(), x.double()) - prob.b.double()
+    rel = (r.flatten(1).norm(dim=1) / prob.b.double().flatten(1).norm(dim=1)).max().item()
     nfail = int((info != 0).sum())
 
     # ---- end to end through the public host-buffer entry point (pinned host in, host out)
     e2e = None
-    if not args.no_e2e:
+    if on_gpu and not args.no_e2e:
+        import paper_2601_03754_b200 as btd
+
         ws_h = btd.HostWorkspace(plan, device=dev)
-        hD, hE, hb = D.cpu().pin_memory(), E.cpu().pin_memory(), b.cpu().pin_memory()
-        with torch.cuda.stream(stream):
+        hD, hE, hb = prob.D.cpu().pin_memory(), prob.E.cpu().pin_memory(), prob.b.cpu().pin_memory()
+        btd.factor_solve_host(hD, hE, hb, ws_h, chunks=args.e2e_chunks, stream=stream)
+        stream.synchronize()
+        barrier()
+        e0 = clock.mark()
+        for _ in range(args.e2e_steps):
             btd.factor_solve_host(hD, hE, hb, ws_h, chunks=args.e2e_chunks, stream=stream)
+        e1 = clock.mark()
         stream.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        with torch.cuda.stream(stream):
-            for _ in range(args.e2e_steps):
-                btd.factor_solve_host(hD, hE, hb, ws_h, chunks=args.e2e_chunks, stream=stream)
-        e1.record(stream)
-        stream.synchronize()
-        t_e2e = e0.elapsed_time(e1) / 1e3
-        h2d = hD.numel() * 4 + hE.numel() * 4 + hb.numel() * 4
-        d2h = (Dhat.numel() + C.numel() + x.numel()) * 4 + info.numel() * 4
-        e2e = dict(t=t_e2e, steps=args.e2e_steps, h2d=h2d, d2h=d2h)
+        h2d = (hD.numel() + hE.numel() + hb.numel()) * W_BYTES
+        d2h = (Dhat.numel() + C.numel() + x.numel()) * W_BYTES + info.numel() * 4
+        e2e = dict(t=clock.ms(e0, e1) / 1e3, steps=args.e2e_steps, h2d=h2d, d2h=d2h)
         del ws_h
 
-    # ---- gather per-rank numbers (after timing; NCCL all_gather of a few floats)
-    stats = torch.tensor([t_total, statistics.mean(kern_ms), rel, float(nfail), e2e["t"] if e2e else 0.0],
-                         dtype=torch.float64, device=dev)
-    allst = shard.gather_stats(stats, max(ws, 1)).cpu()
-    if rank != 0:
-        torch.distributed.destroy_process_group()
-        return
-    agg = shard.aggregate(allst, B, args.steps)
-    t_max = agg["seconds_max"]
-    kern_avg_ms = agg["kernel_ms_max"]
+    stats = torch.tensor([t_total, statistics.mean(kern_ms), rel, float(nfail), e2e["t"] if e2e else 0.0,
+                          float(B)], dtype=torch.float64)
+    return dict(stats=stats, e2e=e2e, clocks=clk.summary(), plan=plan, first=first, count=B)
+
+
+def build_line(args, agg: dict, local: dict, pk: dict | None = None) -> dict:
+    """Rank 0's JSON line from the aggregated statistics (shard.aggregate) and rank 0's extras."""
+    pk = pk or _peaks()
     n = agg["world"]
-    value = agg["systems_per_s"]
+    per_step = agg["systems_per_step"]
+    per_rank_max = max(int(local["count"]), 1)
     ab = algorithmic_bytes_per_system()
-    pk = _peaks()
-    achieved = ab["total"] * B / (kern_avg_ms / 1e3) / 1e9
-    trafficpl = _ncu_traffic()
+    kern_avg_ms = agg["kernel_ms_max"]
+    achieved = ab["total"] * local["count"] / (kern_avg_ms / 1e3) / 1e9 if kern_avg_ms > 0 else None
+    plan = local.get("plan")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (btdgen kalman, seeded, on device)",
-        "config": {"workload": "c5 batched MPC-for-RL: 8192 independent SPD block-tridiagonal systems per GPU, "
-                               "fp32, n=12, N=128, m=1 (BASELINE.json configs[4])",
-                   "batch_per_gpu": B, "global_batch": B * n, "N": N_BLK, "n": N_SZ, "m": M_RHS,
+        "metric": metric_name(args.scaling), "value": agg["systems_per_s"], "unit": UNIT, "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": agg["seconds_max"] / args.steps * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (btdgen kalman, seeded, on device)",
+        "config": {"workload": "c5 batched MPC-for-RL: independent SPD block-tridiagonal systems, fp32, n=12, "
+                               "N=128, m=1 (BASELINE.json configs[4])",
+                   "global_batch": per_step, "batch_per_gpu": per_rank_max if per_step % n == 0 else
+                   f"{per_step // n}-{-(-per_step // n)}", "N": N_BLK, "n": N_SZ, "m": M_RHS,
+                   "partition": "contiguous global-index slices [r*B/G,(r+1)*B/G)" if args.scaling == "strong"
+                   else "B systems per rank, rank r owns [r*B,(r+1)*B)",
                    "parallelism": f"dp{n} (independent systems, no data-path collective)",
-                   "l2": "inputs (1.25 GB/GPU) and outputs larger than L2 (126 MB): no flush needed",
-                   "variant": plan.variant},
-        "us_per_system": t_max / args.steps / B * 1e6,
-        "gpu_launches": launches,
+                   "l2": "inputs (1.25 GB at 8192 systems) and outputs exceed L2 (126 MB): no flush needed",
+                   "variant": getattr(plan, "variant", None)},
+        "us_per_system": agg["seconds_max"] / args.steps / per_step * 1e6 * n,
+        "gpu_launches": args.steps * (plan.launches("factor_solve") if hasattr(plan, "launches") else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm"], "traffic": trafficpl,
-                     "algorithmic_bytes_per_launch": ab["total"] * B, "peak_source": pk["src"],
+                     "frac": achieved / pk["hbm"] if achieved else None,
+                     "traffic": _ncu_traffic(local["count"]),
+                     "algorithmic_bytes_per_launch": ab["total"] * local["count"], "peak_source": pk["src"],
                      "kernel": "btd_fused_r_kernel<float,12,4,32,true,true,1,true>",
                      "kernel_ms_avg": kern_avg_ms},
         "flops_per_system": algorithmic_flops_per_system(),
         "check": {"max_rel_residual_fp64": agg["max_rel_residual"], "failed_systems": agg["failed_systems"]},
-        "clocks": clk.summary(),
+        "clocks": local["clocks"],
     }
+    e2e = local.get("e2e")
     if e2e:
-        t_e2e_max = agg["e2e_seconds_max"]
-        line["e2e"] = {"value": n * B * e2e["steps"] / t_e2e_max, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
-                       "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"], "chunks": args.e2e_chunks,
+        line["e2e"] = {"value": per_step * e2e["steps"] / agg["e2e_seconds_max"], "unit": UNIT,
+                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"],
+                       "chunks": args.e2e_chunks,
                        "api": "btd_factor_solve_host (pinned host buffers, copies inside the timed region)"}
-    if not args.no_cpu_baseline:
-        cb = cpu_oracle_rate(args.cpu_sample, steps=1)
+    return line
+
+
+def run_ours(args):
+    from paper_2601_03754_b200 import shard
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        barrier = dist.barrier
+    else:
+        barrier = None
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    res = run_rank(args, rank, ws, dev, barrier=barrier)
+    # ---- gather per-rank numbers (after timing; one NCCL all_gather of a few floats)
+    allst = shard.gather_stats(res["stats"].to(dev), ws).cpu()
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return
+    agg = shard.aggregate(allst, args.steps)
+    line = build_line(args, agg, res)
+    if not args.no_cpu_baseline and ws == 1:
+        cb = cpu_oracle_rate(args.cpu_sample)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-    if args.latency:
+    if args.latency and ws == 1:
         line["latency_us"] = _latency_sweep(dev)
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=B_PER_GPU)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--batch", type=int, default=B_TOTAL,
+                    help="systems in total (strong) or per rank (weak)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
@@ -373,9 +525,17 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1024)
     ap.add_argument("--latency", action="store_true", default=True)
     ap.add_argument("--no-latency", dest="latency", action="store_false")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    return args
+
+
+def main():
+    args = parse_args()
+    ws, _, _ = _dist()
+    if args.gpus > 1 and ws == 1 and "TORCHELASTIC_RUN_ID" not in os.environ:
+        _respawn_under_torchrun(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

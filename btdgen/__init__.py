@@ -7,8 +7,12 @@ holds none of the factorization/solve arithmetic of the method (SURVEY.md
 
 Randomness is a counter-based hash (``lowbias32`` mixing, integer-exact in
 int64 torch arithmetic), keyed by ``(config seed, global system index,
-element counter)``. The same system index therefore yields bit-identical
-inputs on CPU and GPU and for any sharding of a batch across ranks.
+element counter)``. The random BITS are therefore identical on CPU and GPU
+and for any sharding of a batch across ranks. The floating-point values built
+from them are bit-identical under any sharding on ONE device type; across CPU
+and GPU they agree only to rounding (``kalman`` uses ``torch.linalg.qr`` and
+matmuls, and the Box-Muller transform uses log/cos, whose last bits differ
+between the CPU and CUDA libraries).
 
 Generators:
 

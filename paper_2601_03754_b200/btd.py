@@ -136,25 +136,40 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else _vp(t.data_ptr())
 
 
-def _stream(stream) -> _vp:
+def _stream(stream, device: torch.device) -> _vp:
+    """The stream to launch on: the caller's (must belong to ``device``) or ``device``'s current one."""
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
+    elif stream.device != device:
+        raise ValueError(f"stream is on {stream.device}, tensors on {device}")
     return _vp(stream.cuda_stream)
 
 
-def _check_in(name, t, shape, dtype):
+def _check_in(name, t, shape, dtype, device: torch.device | None = None, align: int = 16):
+    """Every buffer handed to the library (inputs AND caller-supplied outputs): a contiguous CUDA
+    tensor of the plan's shape and dtype, aligned for the kernels' vector accesses, on ``device``."""
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
         raise BtdError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device} (all tensors must share one device)")
     if t.dtype != dtype:
         raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
     if tuple(t.shape) != tuple(shape):
         raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
-    if t.data_ptr() % 16:
-        raise ValueError(f"{name} must be 16-byte aligned")
+    if t.data_ptr() % align:
+        raise ValueError(f"{name} must be {align}-byte aligned")
+
+
+def _check_host(name, t, shape, dtype):
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise ValueError(f"{name} must be a host tensor")
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous {dtype} host tensor of shape {tuple(shape)}, got "
+                         f"{t.dtype} {tuple(t.shape)}")
 
 
 def _plan_for(D: torch.Tensor, m: int, plan: Plan | None, variant: str) -> Plan:
@@ -177,16 +192,21 @@ def factor(D: torch.Tensor, E: torch.Tensor, plan: Plan | None = None, variant: 
     """btd_factor: returns (Dhat, C, info). D [B,N,n,n], E [B,N-1,n,n] on the GPU."""
     p = _plan_for(D, 1 if plan is None else plan.m, plan, variant)
     sh = _shapes(p)
-    _check_in("D", D, sh["D"], p.dtype)
-    _check_in("E", E, sh["E"], p.dtype)
+    dev = D.device
+    _check_in("D", D, sh["D"], p.dtype, dev)
+    _check_in("E", E, sh["E"], p.dtype, dev)
     if out is None:
-        Dhat = torch.empty(sh["D"], dtype=p.dtype, device=D.device)
-        C = torch.empty(sh["C"], dtype=p.dtype, device=D.device)
-        info = torch.empty(p.batch, dtype=torch.int32, device=D.device)
+        Dhat = torch.empty(sh["D"], dtype=p.dtype, device=dev)
+        C = torch.empty(sh["C"], dtype=p.dtype, device=dev)
+        info = torch.empty(p.batch, dtype=torch.int32, device=dev)
     else:
         Dhat, C, info = out
-    _check(lib().btd_factor(p.handle, _ptr(D), _ptr(E) if p.N > 1 else None, _ptr(Dhat), _ptr(C), _ptr(info),
-                            _stream(stream)), "btd_factor")
+        _check_in("out Dhat", Dhat, sh["D"], p.dtype, dev)
+        _check_in("out C", C, sh["C"], p.dtype, dev)
+        _check_in("out info", info, (p.batch,), torch.int32, dev, align=4)
+    with torch.cuda.device(dev):
+        _check(lib().btd_factor(p.handle, _ptr(D), _ptr(E) if p.N > 1 else None, _ptr(Dhat), _ptr(C), _ptr(info),
+                                _stream(stream, dev)), "btd_factor")
     return Dhat, C, info
 
 
@@ -195,11 +215,14 @@ def solve(Dhat: torch.Tensor, C: torch.Tensor, b: torch.Tensor, plan: Plan | Non
     """btd_solve: x = Psi^{-1} b from a factor (Dhat, C) of btd_factor."""
     p = _plan_for(Dhat, b.shape[3], plan, variant)
     sh = _shapes(p)
-    _check_in("Dhat", Dhat, sh["D"], p.dtype)
-    _check_in("C", C, sh["C"], p.dtype)
-    _check_in("b", b, sh["b"], p.dtype)
+    dev = Dhat.device
+    _check_in("Dhat", Dhat, sh["D"], p.dtype, dev)
+    _check_in("C", C, sh["C"], p.dtype, dev)
+    _check_in("b", b, sh["b"], p.dtype, dev)
     x = torch.empty_like(b) if out is None else out
-    _check(lib().btd_solve(p.handle, _ptr(Dhat), _ptr(C), _ptr(b), _ptr(x), _stream(stream)), "btd_solve")
+    _check_in("out x", x, sh["b"], p.dtype, dev)
+    with torch.cuda.device(dev):
+        _check(lib().btd_solve(p.handle, _ptr(Dhat), _ptr(C), _ptr(b), _ptr(x), _stream(stream, dev)), "btd_solve")
     return x
 
 
@@ -208,18 +231,24 @@ def factor_solve(D: torch.Tensor, E: torch.Tensor, b: torch.Tensor, plan: Plan |
     """btd_factor_solve: returns (Dhat, C, x, info)."""
     p = _plan_for(D, b.shape[3], plan, variant)
     sh = _shapes(p)
-    _check_in("D", D, sh["D"], p.dtype)
-    _check_in("E", E, sh["E"], p.dtype)
-    _check_in("b", b, sh["b"], p.dtype)
+    dev = D.device
+    _check_in("D", D, sh["D"], p.dtype, dev)
+    _check_in("E", E, sh["E"], p.dtype, dev)
+    _check_in("b", b, sh["b"], p.dtype, dev)
     if out is None:
-        Dhat = torch.empty(sh["D"], dtype=p.dtype, device=D.device)
-        C = torch.empty(sh["C"], dtype=p.dtype, device=D.device)
-        x = torch.empty(sh["b"], dtype=p.dtype, device=D.device)
-        info = torch.empty(p.batch, dtype=torch.int32, device=D.device)
+        Dhat = torch.empty(sh["D"], dtype=p.dtype, device=dev)
+        C = torch.empty(sh["C"], dtype=p.dtype, device=dev)
+        x = torch.empty(sh["b"], dtype=p.dtype, device=dev)
+        info = torch.empty(p.batch, dtype=torch.int32, device=dev)
     else:
         Dhat, C, x, info = out
-    _check(lib().btd_factor_solve(p.handle, _ptr(D), _ptr(E) if p.N > 1 else None, _ptr(b), _ptr(Dhat),
-                                  _ptr(C), _ptr(x), _ptr(info), _stream(stream)), "btd_factor_solve")
+        _check_in("out Dhat", Dhat, sh["D"], p.dtype, dev)
+        _check_in("out C", C, sh["C"], p.dtype, dev)
+        _check_in("out x", x, sh["b"], p.dtype, dev)
+        _check_in("out info", info, (p.batch,), torch.int32, dev, align=4)
+    with torch.cuda.device(dev):
+        _check(lib().btd_factor_solve(p.handle, _ptr(D), _ptr(E) if p.N > 1 else None, _ptr(b), _ptr(Dhat),
+                                      _ptr(C), _ptr(x), _ptr(info), _stream(stream, dev)), "btd_factor_solve")
     return Dhat, C, x, info
 
 
@@ -230,6 +259,9 @@ class HostWorkspace:
         sh = _shapes(plan)
         dt = plan.dtype
         self.plan = plan
+        self.device = torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.dev = {k: torch.empty(sh[k2], dtype=dt, device=device)
                     for k, k2 in [("D", "D"), ("E", "E"), ("b", "b"), ("Dhat", "D"), ("C", "C"), ("x", "b")]}
         self.dev["info"] = torch.empty(plan.batch, dtype=torch.int32, device=device)
@@ -242,14 +274,16 @@ def factor_solve_host(D: torch.Tensor, E: torch.Tensor, b: torch.Tensor, ws: Hos
                       stream=None):
     """btd_factor_solve_host: host (pinned) D, E, b in; host Dhat, C, x, info out (all async on stream)."""
     p = ws.plan
+    sh = _shapes(p)
     for name, t in (("D", D), ("E", E), ("b", b)):
-        if t.is_cuda or not t.is_contiguous() or t.dtype != p.dtype:
-            raise ValueError(f"{name} must be a contiguous host tensor of dtype {p.dtype}")
+        _check_host(name, t, sh[name], p.dtype)
     d, h = ws.dev, ws.host
-    _check(lib().btd_factor_solve_host(
-        p.handle, _ptr(D), _ptr(E) if p.N > 1 else None, _ptr(b), _ptr(h["Dhat"]), _ptr(h["C"]), _ptr(h["x"]),
-        _ptr(h["info"]), _ptr(d["D"]), _ptr(d["E"]) if p.N > 1 else None, _ptr(d["b"]), _ptr(d["Dhat"]),
-        _ptr(d["C"]), _ptr(d["x"]), _ptr(d["info"]), int(chunks), _stream(stream)), "btd_factor_solve_host")
+    with torch.cuda.device(ws.device):
+        _check(lib().btd_factor_solve_host(
+            p.handle, _ptr(D), _ptr(E) if p.N > 1 else None, _ptr(b), _ptr(h["Dhat"]), _ptr(h["C"]), _ptr(h["x"]),
+            _ptr(h["info"]), _ptr(d["D"]), _ptr(d["E"]) if p.N > 1 else None, _ptr(d["b"]), _ptr(d["Dhat"]),
+            _ptr(d["C"]), _ptr(d["x"]), _ptr(d["info"]), int(chunks), _stream(stream, ws.device)),
+            "btd_factor_solve_host")
     return h["Dhat"], h["C"], h["x"], h["info"]
 
 

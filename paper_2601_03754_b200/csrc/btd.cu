@@ -4,13 +4,17 @@
 // (PAPER.md:569), slot offsets off(l) = sum_{l'<l} (floor(N/2^(l'-1)) - 1), the compiled block
 // size NB >= n (identity padding), the team width and the kernel variant. No device tables:
 // every index is closed form in (level, column) and passed as kernel arguments.
-#include <vector>
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <utility>
+#include <vector>
 
 #include "btd_internal.h"
 #include "btd_persist.cuh"
@@ -25,6 +29,27 @@ btd_status btd::record_cuda_error(cudaError_t e) {
     return BTD_ECUDA;
 }
 static btd_status cuda_fail(cudaError_t e) { return record_cuda_error(e); }
+
+btd_status btd::ensure_smem_attr(const void *kern, size_t bytes) {
+    if (bytes <= 48 * 1024) return BTD_OK;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t &have = done[{dev, kern}];
+    if (bytes <= have) return BTD_OK;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return cuda_fail(e);
+    have = bytes;
+    return BTD_OK;
+}
+
+// Device buffers are read and written with 16-byte vector accesses (LDGSTS / LDG.128 / STG.128)
+// from their base address; the per-system strides are handled inside the kernels.
+static bool al16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+static bool al4(const void *p) { return ((uintptr_t)p & 3u) == 0; }
 
 static const int kSizes[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
 
@@ -72,6 +97,39 @@ static btd_status run(const btd_plan *p, int op, const void *D, const void *E, c
     }
     if (p->dtype == BTD_F32) return run_dtype<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
     return run_dtype<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+}
+
+// Streams and events of btd_factor_solve_host, created once per (host thread, device) and kept for
+// the thread's lifetime (one thread's calls are issued in order, so reusing an event is safe: each
+// cudaStreamWaitEvent captures the record made just before it).
+struct HostPipe {
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t fork = nullptr, done = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_out;
+};
+
+static btd_status host_pipe(int nch, HostPipe **out) {
+    static thread_local std::map<int, HostPipe> pipes;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    HostPipe &hp = pipes[dev];
+    if (!hp.up && (e = cudaStreamCreateWithFlags(&hp.up, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e);
+    if (!hp.down && (e = cudaStreamCreateWithFlags(&hp.down, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e);
+    if (!hp.fork && (e = cudaEventCreateWithFlags(&hp.fork, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e);
+    if (!hp.done && (e = cudaEventCreateWithFlags(&hp.done, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e);
+    while ((int)hp.ev_in.size() < nch) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e);
+        if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) {
+            cudaEventDestroy(a);
+            return cuda_fail(e);
+        }
+        hp.ev_in.push_back(a);
+        hp.ev_out.push_back(b);
+    }
+    *out = &hp;
+    return BTD_OK;
 }
 
 // ------------------------------------------------------------------ C ABI
@@ -125,6 +183,10 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         // few independent systems with enough level-1 columns to spread over the SMs: latency path
         const bool wide_ok = NB > 0 && wsm <= kMaxSmem && batch * ((N + 1) / 2) <= 4 * 148 && N >= 16;
         p->variant = wide_ok ? BTD_VARIANT_WIDE : fits ? BTD_VARIANT_FUSED : BTD_VARIANT_PERSIST;
+        if (p->variant == BTD_VARIANT_PERSIST && NB < 0 && psm > kMaxSmem) {  // e.g. n = 128 fp64 with m >= 32
+            delete p;
+            return BTD_EUNSUPPORTED;
+        }
     } else {
         p->variant = variant;
     }
@@ -177,17 +239,20 @@ int64_t btd_plan_smem_bytes(const btd_plan *p) {
 btd_status btd_factor(const btd_plan *p, const void *D, const void *E, void *Dhat, void *C, int32_t *info,
                       void *stream) {
     if (!p || !D || !Dhat || (!C && p->geo.nC > 0) || !info || (p->N > 1 && !E)) return BTD_EINVAL;
+    if (!al16(D) || !al16(E) || !al16(Dhat) || !al16(C) || !al4(info)) return BTD_EINVAL;
     return run(p, 0, D, E, nullptr, Dhat, C, nullptr, info, 0, p->batch, stream);
 }
 
 btd_status btd_solve(const btd_plan *p, const void *Dhat, const void *C, const void *b, void *x, void *stream) {
     if (!p || !Dhat || (!C && p->geo.nC > 0) || !b || !x) return BTD_EINVAL;
+    if (!al16(Dhat) || !al16(C) || !al16(b) || !al16(x)) return BTD_EINVAL;
     return run(p, 1, nullptr, nullptr, b, (void *)Dhat, (void *)C, x, nullptr, 0, p->batch, stream);
 }
 
 btd_status btd_factor_solve(const btd_plan *p, const void *D, const void *E, const void *b, void *Dhat, void *C,
                             void *x, int32_t *info, void *stream) {
     if (!p || !D || !b || !Dhat || (!C && p->geo.nC > 0) || !x || !info || (p->N > 1 && !E)) return BTD_EINVAL;
+    if (!al16(D) || !al16(E) || !al16(b) || !al16(Dhat) || !al16(C) || !al16(x) || !al4(info)) return BTD_EINVAL;
     return run(p, 2, D, E, b, Dhat, C, x, info, 0, p->batch, stream);
 }
 
@@ -198,6 +263,8 @@ btd_status btd_factor_solve_host(const btd_plan *p, const void *hD, const void *
         chunks < 1)
         return BTD_EINVAL;
     if (p->N > 1 && (!hE || !dE)) return BTD_EINVAL;
+    if (!al16(dD) || !al16(dE) || !al16(db) || !al16(dDhat) || !al16(dC) || !al16(dx) || !al4(dinfo))
+        return BTD_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t w = p->dtype == BTD_F32 ? 4 : 8;
     const size_t nn = (size_t)p->n * p->n;
@@ -208,41 +275,23 @@ btd_status btd_factor_solve_host(const btd_plan *p, const void *hD, const void *
     // Three-stage pipeline: host->device copies on stream `up`, compute on the caller's stream,
     // device->host copies on stream `down` (the two copy directions run on separate copy engines),
     // chained per slice by events; the caller's stream finally waits for `down`, so the call stays
-    // asynchronous and ordered on `stream`. Streams/events are released by the driver once the
-    // queued work completes (cudaStreamDestroy / cudaEventDestroy semantics).
-    cudaStream_t up = nullptr, down = nullptr;
-    cudaEvent_t fork = nullptr, done = nullptr;
-    std::vector<cudaEvent_t> ev_in(nch, nullptr), ev_out(nch, nullptr);
+    // asynchronous and ordered on `stream`. The two streams and the events are created once per
+    // (host thread, device) and reused by every later call (HostPipe).
+    HostPipe *hp = nullptr;
+    btd_status rs = host_pipe(nch, &hp);
+    if (rs != BTD_OK) return rs;
+    cudaStream_t up = hp->up, down = hp->down;
     cudaError_t e = cudaSuccess;
-    auto cleanup = [&]() {
-        for (auto &x : ev_in)
-            if (x) cudaEventDestroy(x);
-        for (auto &x : ev_out)
-            if (x) cudaEventDestroy(x);
-        if (fork) cudaEventDestroy(fork);
-        if (done) cudaEventDestroy(done);
-        if (up) cudaStreamDestroy(up);
-        if (down) cudaStreamDestroy(down);
-    };
 #define CK(call)                         \
     do {                                 \
         e = (call);                      \
         if (e != cudaSuccess) {          \
-            cleanup();                   \
             return cuda_fail(e);         \
         }                                \
     } while (0)
-    CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    for (int c = 0; c < nch; ++c) {
-        CK(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
-    }
-    CK(cudaEventRecord(fork, st));  // everything queued on `stream` before this call comes first
-    CK(cudaStreamWaitEvent(up, fork, 0));
-    CK(cudaStreamWaitEvent(down, fork, 0));
+    CK(cudaEventRecord(hp->fork, st));  // everything queued on `stream` before this call comes first
+    CK(cudaStreamWaitEvent(up, hp->fork, 0));
+    CK(cudaStreamWaitEvent(down, hp->fork, 0));
     for (int c = 0; c < nch; ++c) {
         const int64_t s0 = c * per;
         const int64_t cnt = (p->batch - s0) < per ? (p->batch - s0) : per;
@@ -250,25 +299,21 @@ btd_status btd_factor_solve_host(const btd_plan *p, const void *hD, const void *
         if (sE)
             CK(cudaMemcpyAsync((char *)dE + s0 * sE, (const char *)hE + s0 * sE, cnt * sE, cudaMemcpyHostToDevice, up));
         CK(cudaMemcpyAsync((char *)db + s0 * sb, (const char *)hb + s0 * sb, cnt * sb, cudaMemcpyHostToDevice, up));
-        CK(cudaEventRecord(ev_in[c], up));
-        CK(cudaStreamWaitEvent(st, ev_in[c], 0));
-        btd_status rs = run(p, 2, dD, dE, db, dDhat, dC, dx, dinfo, s0, cnt, stream);
-        if (rs != BTD_OK) {
-            cleanup();
-            return rs;
-        }
-        CK(cudaEventRecord(ev_out[c], st));
-        CK(cudaStreamWaitEvent(down, ev_out[c], 0));
+        CK(cudaEventRecord(hp->ev_in[c], up));
+        CK(cudaStreamWaitEvent(st, hp->ev_in[c], 0));
+        rs = run(p, 2, dD, dE, db, dDhat, dC, dx, dinfo, s0, cnt, stream);
+        if (rs != BTD_OK) return rs;
+        CK(cudaEventRecord(hp->ev_out[c], st));
+        CK(cudaStreamWaitEvent(down, hp->ev_out[c], 0));
         CK(cudaMemcpyAsync((char *)hDhat + s0 * sD, (const char *)dDhat + s0 * sD, cnt * sD, cudaMemcpyDeviceToHost, down));
         if (sC)
             CK(cudaMemcpyAsync((char *)hC + s0 * sC, (const char *)dC + s0 * sC, cnt * sC, cudaMemcpyDeviceToHost, down));
         CK(cudaMemcpyAsync((char *)hx + s0 * sb, (const char *)dx + s0 * sb, cnt * sb, cudaMemcpyDeviceToHost, down));
         CK(cudaMemcpyAsync(hinfo + s0, dinfo + s0, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost, down));
     }
-    CK(cudaEventRecord(done, down));
-    CK(cudaStreamWaitEvent(st, done, 0));
+    CK(cudaEventRecord(hp->done, down));
+    CK(cudaStreamWaitEvent(st, hp->done, 0));
 #undef CK
-    cleanup();
     return BTD_OK;
 }
 

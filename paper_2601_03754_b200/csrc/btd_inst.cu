@@ -19,15 +19,9 @@ static btd_status launch_fused_mr(const btd_plan *p, const T *D, const T *E, con
     else
         kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
     const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
-    // opt in to > 48 KB dynamic smem once per size -- per KERNEL: the exact-n (EX) and padded
-    // FUSED-R instantiations are two kernels behind one launcher
-    const int kx = (R && p->n == NB) ? 1 : 0;
-    static size_t attr_bytes[2] = {0, 0};
-    if (smem > 48 * 1024 && smem > attr_bytes[kx]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_fail(e);
-        attr_bytes[kx] = smem;
-    }
+    // opt in to > 48 KB dynamic smem per (device, KERNEL): the exact-n (EX) and padded FUSED-R
+    // instantiations are two kernels behind one launcher
+    if (btd_status rs = ensure_smem_attr((const void *)kern, smem); rs != BTD_OK) return rs;
     for (int64_t s0 = 0; s0 < count; s0 += (1ll << 30)) {
         const int64_t cnt = (count - s0) < (1ll << 30) ? (count - s0) : (1ll << 30);
         kern<<<(unsigned)cnt, NT * TS, smem, st>>>(D, E, b, Dhat, C, x, info, p->geo, (int)(sys0 + s0));
@@ -100,12 +94,7 @@ static btd_status launch_persist_team(const btd_plan *p, const T *D, const T *E,
     using Cfg = PTeamCfg<T, NB>;
     auto kern = btd_persist_team_kernel<T, NB, FACT, SOLVE>;
     const size_t smem = Cfg::BYTES;
-    static size_t attr_bytes = 0;
-    if (smem > 48 * 1024 && smem > attr_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_fail(e);
-        attr_bytes = smem;
-    }
+    if (btd_status rs = ensure_smem_attr((const void *)kern, smem); rs != BTD_OK) return rs;
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

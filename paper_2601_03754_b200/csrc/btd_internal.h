@@ -20,6 +20,11 @@ struct btd_plan {
 namespace btd {
 btd_status record_cuda_error(cudaError_t e);
 
+// Opt kernel `kern` in to `bytes` of dynamic shared memory on the CURRENT device (the attribute is
+// per device context). Remembered per (device, kernel) under a mutex, so concurrent callers and
+// processes driving several GPUs each set it once per device.
+btd_status ensure_smem_attr(const void *kern, size_t bytes);
+
 template <int NB>
 struct TeamShape {
     static constexpr int TS = NB <= 1 ? 1 : NB <= 2 ? 2 : NB <= 4 ? 4 : NB <= 8 ? 8 : NB <= 16 ? 16 : 32;

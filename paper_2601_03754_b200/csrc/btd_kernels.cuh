@@ -38,9 +38,6 @@
 #ifndef BTD_FR_MINB
 #define BTD_FR_MINB 2
 #endif
-#ifndef BTD_SPLIT
-#define BTD_SPLIT 0  // measured: 3.41M (split) vs 3.62M systems/s (c5); see DESIGN.md
-#endif
 namespace btd {
 
 struct Geo {
@@ -392,21 +389,9 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
         const int s = 1 << (l - 1);
         const int ncols = ((N / s) + 1) / 2;
         const long long offL = g.off[l - 1];
-        // Upper levels (fewer columns than teams, backward cache active): G warps share each column
-        // op by role. Role 0 (the lead) runs the POTRF+TRSM sweep and writes D^, C_r, C_l to the
-        // shared-memory cache; after one CTA barrier the other roles read C_r, C_l from there:
-        //   role 0: POTRF+TRSM, D^/C_r (and, G = 2, C_l) stores, forward-solve push, l.11 downdate
-        //   role 1: fill GEMM (l.13) + C_l^T C_l and the phase-Y left pushes (l.7/l.9)
-        //   role 2 (G = 4): C_l stores; role 3 idle.
-        // The level's critical path: one sweep + max(role 0's tail, role 1's GEMMs).
-        const bool splitok = BTD_SPLIT && FACT && SOLVE && l >= bc.LC;
-        const int G = (splitok && ncols <= TPW) ? 4 : (splitok && ncols <= 2 * TPW) ? 2 : 1;
-        const int GC = NWARP / G;  // warps per role = column groups
-        const int role = warp / GC;
-        const bool doDR = role == 0, doCl = (G == 4) ? role == 2 : role == 0, doFSL = (G == 1) || role == 1;
         for (int j0 = 0; j0 < ncols; j0 += NT) {
-            const int j = j0 + (warp % GC) * TPW + team % TPW;
-            const bool wact = j0 + (warp % GC) * TPW < ncols;
+            const int j = j0 + team;
+            const bool wact = j0 + warp * TPW < ncols;
             const bool act = j < ncols;
             const int c = act ? s * (2 * j + 1) : s;  // inactive teams shadow a valid column, store nothing
             const bool hasL = act && c > s;
@@ -421,7 +406,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                 T yv[NB];
                 T cr[RPL][NB];
                 BTD_SUB_INIT();
-                if (FACT && doDR) {
+                if (FACT) {
                     // -- a4 operands: couplings (row q+TS t of the right one, column q+TS t of the
                     // left one); level 1 reads them from HBM, later levels from the fill slots
                     if (l == 1) {
@@ -457,19 +442,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                     }
                     g_store_rows<T, NB, TS, RPL>(Dh + (size_t)(c - 1) * nn, a, n, ln, act);
                     g_store_rows<T, NB, TS, RPL>(Cs + (offL + c / s - 1) * nn, cr, n, ln, hasR);
-                    if (doCl) g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
-                }
-                if (FACT && G > 1) {
-                    // the lead has read D~_c (role 1 overwrites its slot with the fill) and written
-                    // D^, C_r, C_l to the cache (all warps are active at a split level; G is uniform)
-                    __syncthreads();
-                    if (!doDR) {
-                        const int qb = bc.base(N, l);
-                        const T *pd = slots + (size_t)bc.slot(qb + (act ? j : 0)) * BLK;
-                        s_load_rows<T, NB, TS, RPL>(cr, hasR ? slots + (size_t)bc.slot(qb + ncols + c / s - 1) * BLK : pd, ln);
-                        s_load_cols<T, NB, TS, RPL>(cl, hasL ? slots + (size_t)bc.slot(qb + ncols + c / s - 2) * BLK : pd, ln);
-                        if (doCl) g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
-                    }
+                    g_store_cols<T, NB, TS, RPL>(Cs + (offL + c / s - 2) * nn, cl, n, ln, hasL);
                 }
                 if constexpr (!FACT && !FY) {
                     load_L_full<T, NB>(Lf, Linv, Dh + (size_t)(c - 1) * nn, n);
@@ -479,7 +452,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                 }
                 BTD_SUB(l >= 3, 21);
                 // -- a6: y_c <- D^^{-1} y_c (redundantly in every lane of the team), y_{c+s} -= C_r y_c
-                if (SOLVE && doDR) {
+                if (SOLVE) {
                     for (int q = 0; q < m; ++q) {
                         T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                         if constexpr (!FY) {
@@ -502,7 +475,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                 BTD_SUB(l >= 3, 22);
                 if (FACT) {
                     // -- a2 (right): D~_{c+s} -= C_r C_r^T   (rows of C_r exchanged by shuffles)
-                    if (doDR) {
+                    {
                         T SR[RPL][NB];
                         set_zero<T, NB, RPL>(SR);
 #pragma unroll
@@ -529,7 +502,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                     }
                     BTD_SUB(l >= 3, 23);
                     // -- a5 fill -C_r C_l -> slot[c], and C_l^T C_l for phase Y (columns of C_l shuffled)
-                    if (doFSL) {
+                    {
                         T F[RPL][NB];
                         set_zero<T, NB, RPL>(F);
                         set_zero<T, NB, RPL>(SL);
@@ -552,7 +525,7 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
             __syncthreads();
             BTD_STAMP(l < 11 ? 5 + l : 1);
             // ---- phase Y: left pushes (deferred left-looking part of Alg. 4, l.7/l.9)
-            if (wact && hasL && doFSL) {
+            if (wact && hasL) {
                 if (FACT) {
                     T *p = slots + (size_t)(c - s - 1) * BLK;
 #pragma unroll

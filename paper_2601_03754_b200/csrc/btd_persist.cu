@@ -11,12 +11,7 @@ btd_status run_persist(const btd_plan *p, int op, const void *D, const void *E, 
     const int n = (int)p->n, m = (int)p->m, N = (int)p->N;
     const size_t smem = PersistSmem<T>::bytes(n, m);
     auto kern = btd_persist_kernel<T>;
-    static size_t attr_bytes = 0;
-    if (smem > 48 * 1024 && smem > attr_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return record_cuda_error(e);
-        attr_bytes = smem;
-    }
+    if (btd_status rs = ensure_smem_attr((const void *)kern, smem); rs != BTD_OK) return rs;
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -51,12 +46,7 @@ static btd_status launch_wide(const btd_plan *p, int op, const void *D, const vo
     const int n = (int)p->n, m = (int)p->m, N = (int)p->N;
     const size_t smem = WideSmem<T>::bytes(n, m);
     auto kern = btd_wide_kernel<T, NB>;
-    static size_t attr_bytes = 0;
-    if (smem > 48 * 1024 && smem > attr_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return record_cuda_error(e);
-        attr_bytes = smem;
-    }
+    if (btd_status rs = ensure_smem_attr((const void *)kern, smem); rs != BTD_OK) return rs;
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -97,3 +97,46 @@ def test_status_strings():
     L = btd.lib()
     assert L.btd_status_string(0) == b"BTD_OK"
     assert b"invalid" in L.btd_status_string(1)
+
+
+def test_auto_rejects_oversized_persist_at_plan_time():
+    """n = 128 fp64 with many right-hand sides needs more than 227 KB of shared memory in PERSIST:
+    AUTO refuses at plan creation (BTD_EUNSUPPORTED) instead of failing at every launch."""
+    import ctypes
+
+    L = btd.lib()
+    h = ctypes.c_void_p()
+    assert L.btd_plan_create(ctypes.byref(h), 256, 128, 1, 64, 1) == 4
+    assert L.btd_plan_create(ctypes.byref(h), 256, 128, 1, 1, 1) == 0
+    L.btd_plan_destroy(h)
+
+
+def test_misaligned_device_pointers_are_rejected_before_launch():
+    """Every device buffer is accessed with 16-byte vector operations from its base: a misaligned
+    pointer returns BTD_EINVAL (checked on the host, before any CUDA call -- no GPU needed)."""
+    import ctypes
+
+    L = btd.lib()
+    p = btd.Plan(8, 4, 1, 1, torch.float32)
+    a, mis = ctypes.c_void_p(1 << 20), ctypes.c_void_p((1 << 20) + 4)
+    st = ctypes.c_void_p(0)
+    assert L.btd_factor(p.handle, mis, a, a, a, a, st) == 1
+    assert L.btd_factor(p.handle, a, a, a, mis, a, st) == 1
+    assert L.btd_factor(p.handle, a, a, a, a, ctypes.c_void_p((1 << 20) + 2), st) == 1
+    assert L.btd_solve(p.handle, a, a, mis, a, st) == 1
+    assert L.btd_factor_solve(p.handle, a, a, a, a, a, mis, a, st) == 1
+    args = [a] * 7 + [a, a, a, a, a, mis, a]
+    assert L.btd_factor_solve_host(p.handle, *args, 1, st) == 1
+
+
+def test_binding_checks_caller_supplied_outputs():
+    """out= buffers go through the same shape/dtype/device checks as the inputs (before any launch)."""
+    D = torch.eye(2, dtype=torch.float64).expand(1, 4, 2, 2).contiguous()
+    E = torch.zeros(1, 3, 2, 2, dtype=torch.float64)
+    b = torch.ones(1, 4, 2, 1, dtype=torch.float64)
+    with pytest.raises((btd.BtdError, ValueError, TypeError)):
+        btd.factor_solve(D, E, b, out=(D, E, b, torch.zeros(1, dtype=torch.int32)))
+    ws_plan = btd.Plan(4, 2, 1, 1, torch.float64)
+    with pytest.raises(ValueError):
+        btd.btd._check_host("D", torch.zeros(1, 4, 2, 3, dtype=torch.float64), (1, 4, 2, 2), torch.float64)
+    assert ws_plan.num_coupling_blocks == 4
