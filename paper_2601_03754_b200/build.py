@@ -44,9 +44,20 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _deps_of(obj: str) -> list[str] | None:
+    """Headers the object was compiled from (nvcc -MD output), or None if unknown."""
+    d = obj[:-2] + ".d"
+    try:
+        txt = open(d).read().replace("\\\n", " ")
+    except OSError:
+        return None
+    parts = txt.split(":", 1)[1].split() if ":" in txt else []
+    return [x for x in parts if os.path.exists(x)]
+
+
 def _compile(args: tuple[str, list[str], str]) -> str:
     src, defs, obj = args
-    cmd = [_nvcc(), *ARCH, *FLAGS, *defs, "-c", src, "-o", obj]
+    cmd = [_nvcc(), *ARCH, *FLAGS, *defs, "-MD", "-MF", obj[:-2] + ".d", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {obj}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
@@ -70,7 +81,11 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, t
         for nb in SIZES:
             units.append((os.path.join(CSRC, "btd_inst.cu"), [f"-DBTD_T={dt}", f"-DBTD_NB={nb}"],
                           os.path.join(OBJ, f"btd_inst_{dt}_{nb}.o")))
-    todo = [u for u in units if force or _stale(u[2], deps)]
+    def stale(u):
+        d = _deps_of(u[2])
+        return _stale(u[2], (d + [u[0]]) if d else deps)
+
+    todo = [u for u in units if force or stale(u)]
     jobs = jobs or max(1, os.cpu_count() or 1)
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
         for (src, defs, obj), msg in zip(todo, ex.map(_compile, todo)):

@@ -149,6 +149,12 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
     btd_plan *p = new (std::nothrow) btd_plan();
     if (!p) return BTD_ENOMEM;
     p->N = N; p->n = n; p->batch = batch; p->m = m; p->dtype = dtype; p->NB = NB;
+    {
+        const char *ev = getenv("BTD_FUSED_R2");  // dev knob for A/B measurements (default on)
+        p->use_r2 = !(ev && ev[0] == '0');
+        const char *mb = getenv("BTD_R2_MINB");
+        p->r2_minb = (mb && mb[0] == '2') ? 2 : 3;
+    }
     int L = 0;
     while ((1ll << L) <= N) ++L;  // floor(log2 N) + 1
     p->L = L;

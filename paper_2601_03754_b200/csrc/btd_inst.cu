@@ -1,5 +1,6 @@
 // btd_inst.cu -- typed launchers; compiled once per (dtype, NB) with -DBTD_T=<float|double> -DBTD_NB=<n>
 // so the 20 instantiations build in parallel (see paper_2601_03754_b200/build.py).
+#include "btd_fused_r2.cuh"
 #include "btd_internal.h"
 #include "btd_persist.cuh"
 
@@ -18,6 +19,20 @@ static btd_status launch_fused_mr(const btd_plan *p, const T *D, const T *E, con
                           : btd_fused_r_kernel<T, NB, TS, NT, FACT, SOLVE, MR, false>;
     else
         kern = btd_fused_kernel<T, NB, TS, NT, FACT, SOLVE, MR>;
+    if constexpr (FACT && SOLVE && MR == 1 && r2_capable<T, NB>()) {
+        if (p->n == NB && p->use_r2) {
+            auto k2 = p->r2_minb == 2 ? btd_fused_r2_kernel<T, NB, TS, NT, 2> : btd_fused_r2_kernel<T, NB, TS, NT, 3>;
+            const size_t sm2 = FusedR2Cfg<T, NB>::bytes((int)p->N);
+            if (btd_status rs = ensure_smem_attr((const void *)k2, sm2); rs != BTD_OK) return rs;
+            for (int64_t s0 = 0; s0 < count; s0 += (1ll << 30)) {
+                const int64_t cnt = (count - s0) < (1ll << 30) ? (count - s0) : (1ll << 30);
+                k2<<<(unsigned)cnt, NT * TS, sm2, st>>>(D, E, b, Dhat, C, x, info, p->geo, (int)(sys0 + s0));
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return cuda_fail(e);
+            }
+            return BTD_OK;
+        }
+    }
     const size_t smem = fused_bytes<T, NB>(p, FACT, SOLVE);
     // opt in to > 48 KB dynamic smem per (device, KERNEL): the exact-n (EX) and padded FUSED-R
     // instantiations are two kernels behind one launcher

@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/btd.h"
-#include "btd_kernels.cuh"
+#include "btd_fused_r2.cuh"
 
 struct btd_plan {
     int64_t N, n, batch, m;
@@ -13,6 +13,8 @@ struct btd_plan {
     int variant;   // BTD_VARIANT_FUSED / BTD_VARIANT_LEVEL
     size_t smem_fs, smem_f, smem_s;  // fused smem bytes: factor+solve, factor, solve
     size_t smem_persist;             // PERSIST kernel dynamic smem bytes
+    int r2_minb;                     // FUSED-R2 min CTAs/SM (register cap): 3 (default) or 2 (env BTD_R2_MINB)
+    bool use_r2;                     // factor+solve, m = 1, n == NB: FUSED-R2 (env BTD_FUSED_R2=0 disables)
     btd::Geo geo;
 };
 
@@ -41,8 +43,24 @@ struct LevelShape {
 
 constexpr size_t kMaxSmem = 227 * 1024 - 64;  // minus the kernel's static shared bytes
 
+// FUSED-R2 (btd_fused_r2.cuh) handles factor+solve with m = 1 for the FUSED-R sizes whose rows
+// are whole 16-byte vectors (fp32 n in {4, 8, 12}, fp64 n in {2, 4, 6, 8}).
+template <typename T, int NB>
+constexpr bool r2_capable() {
+    return FusedRCfg<T, NB>::OK && Dims<T, NB>::LD == NB;
+}
+
 template <typename T, int NB>
 size_t fused_bytes(const btd_plan *p, bool fact, bool solve) {
+    if constexpr (r2_capable<T, NB>()) {
+        if (fact && solve && p->m == 1 && p->n == NB && p->use_r2) {
+            // (N * LD) elements of Y + odd full slots + even padded-lower slots
+            const int N = (int)p->N;
+            const size_t e = (size_t)((N + 1) / 2) * Dims<T, NB>::BLK + (size_t)(N / 2) * PLow<T, NB>::SZ +
+                             (size_t)N * Dims<T, NB>::LD;
+            return e * sizeof(T);
+        }
+    }
     if (FusedRCfg<T, NB>::OK) return FusedRCfg<T, NB>::bytes((int)p->N, (int)p->m, fact, solve);
     return FusedSmem<T, NB, FusedCfg<T, NB>::NT>::bytes((int)p->N, (int)p->m, fact, solve);
 }

@@ -357,7 +357,6 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
     constexpr int LD = Dims<T, NB>::LD, BLK = Dims<T, NB>::BLK;
     constexpr int RPL = NB / TS;
     constexpr int TPW = 32 / TS;
-    constexpr int NWARP = NT * TS / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *slots = reinterpret_cast<T *>(smem_raw);
     __shared__ unsigned s_fail;

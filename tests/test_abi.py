@@ -140,3 +140,71 @@ def test_binding_checks_caller_supplied_outputs():
     with pytest.raises(ValueError):
         btd.btd._check_host("D", torch.zeros(1, 4, 2, 3, dtype=torch.float64), (1, 4, 2, 2), torch.float64)
     assert ws_plan.num_coupling_blocks == 4
+
+
+def _v2(o):
+    return (o & -o).bit_length() - 1
+
+
+def _r2_cache_plan(N):
+    """Host mirror of R2Cache (csrc/btd_fused_r2.cuh): first cached level LC and the odd slot of
+    every cached coupling block, handed out in order of death."""
+    L = N.bit_length()
+    NO = (N + 1) // 2
+    ccount = lambda l: (N >> (l - 1)) - 1
+    group = lambda g: ((NO - 1) >> g) // 2 + ((NO - 1) >> g) % 2
+    LC = L + 1
+    for lc in range(3, L + 1):
+        need, ok = 0, True
+        for l in range(lc, L + 1):
+            need += ccount(l)
+            if need > sum(group(g) for g in range(0, l - 2)):
+                ok = False
+                break
+        if ok:
+            LC = lc
+            break
+    order = []
+    g = 0
+    while len(order) < NO:
+        cnt = group(g)
+        order += [(2 * q + 1) << g for q in range(cnt)]
+        g += 1
+        if g > 40:
+            break
+    return LC, order
+
+
+@pytest.mark.parametrize("N", list(range(1, 70)) + [100, 127, 128, 129, 255, 256, 1000, 1024, 4096])
+def test_fused_r2_slot_schedule_is_race_free(N):
+    """FUSED-R2's shared-memory schedule, simulated level by level on the host: every fill lands in
+    a free odd slot and is read exactly once by the next level's column (Alg. 4 l.13 -> l.10/l.12);
+    backward-cache entries of level l >= LC land in odd slots that are dead for the rest of the
+    factorization (never holding a fill that is still to be read, never overwritten later)."""
+    L = N.bit_length()
+    LC, order = _r2_cache_plan(N)
+    live = {}  # odd slot index -> ("fill", level) or ("cache", level)
+    q = 0
+    for l in range(1, L + 1):
+        s = 1 << (l - 1)
+        cols = list(range(s, N + 1, 2 * s))
+        if l >= LC:  # cache entries of this level: coupling blocks k = 1..N/s-1
+            for _ in range(ccount := (N >> (l - 1)) - 1):
+                o = order[q]
+                assert o not in live, (N, l, o, live.get(o))
+                live[o] = ("cache", l)
+                q += 1
+        for c in cols:
+            hasL, hasR = c > s, c + s <= N
+            if l >= 2:
+                if hasL:
+                    assert live.pop((c - s) // 2) == ("fill", l - 1)
+                if hasR:
+                    assert live.pop(c // 2) == ("fill", l - 1)
+            if hasL and hasR:
+                o = (c - s) // 2  # odd slot of block c - s + 1
+                assert o not in live
+                live[o] = ("fill", l)
+    assert all(v[0] == "cache" for v in live.values())
+    if N == 128:
+        assert LC == 3
