@@ -18,6 +18,7 @@
 
 #include "btd_internal.h"
 #include "btd_persist.cuh"
+#include "btd_persist2.cuh"
 #include "btd_wide.cuh"
 
 using namespace btd;
@@ -154,6 +155,8 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         p->use_r2 = !(ev && ev[0] == '0');
         const char *mb = getenv("BTD_R2_MINB");
         p->r2_minb = (mb && mb[0] == '2') ? 2 : 3;
+        const char *p2 = getenv("BTD_PERSIST2");
+        p->use_persist2 = !(p2 && p2[0] == '0');
     }
     int L = 0;
     while ((1ll << L) <= N) ++L;  // floor(log2 N) + 1
@@ -174,7 +177,10 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
     } else {
         p->smem_fs = p->smem_f = p->smem_s = ~(size_t)0;
     }
-    const size_t psm = NB > 0 ? 0 : (f32 ? PersistSmem<float>::bytes((int)n, (int)m) : PersistSmem<double>::bytes((int)n, (int)m));
+    size_t psm = 0;
+    if (NB < 0)
+        psm = p->use_persist2 ? (f32 ? Persist2Smem<float>::bytes((int)n, (int)m) : Persist2Smem<double>::bytes((int)n, (int)m))
+                              : (f32 ? PersistSmem<float>::bytes((int)n, (int)m) : PersistSmem<double>::bytes((int)n, (int)m));
     const bool fits = p->smem_fs <= kMaxSmem;
     if ((variant == BTD_VARIANT_FUSED && !fits) || (variant == BTD_VARIANT_PERSIST && psm > kMaxSmem)) {
         delete p;

@@ -14,6 +14,7 @@ struct btd_plan {
     size_t smem_fs, smem_f, smem_s;  // fused smem bytes: factor+solve, factor, solve
     size_t smem_persist;             // PERSIST kernel dynamic smem bytes
     int r2_minb;                     // FUSED-R2 min CTAs/SM (register cap): 3 (default) or 2 (env BTD_R2_MINB)
+    bool use_persist2;               // n > 32: PERSIST2 (env BTD_PERSIST2=0 selects the round-1 PERSIST kernel)
     bool use_r2;                     // factor+solve, m = 1, n == NB: FUSED-R2 (env BTD_FUSED_R2=0 disables)
     btd::Geo geo;
 };

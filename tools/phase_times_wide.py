@@ -14,7 +14,7 @@ dt = torch.float32 if sys.argv[3] == "f32" else torch.float64
 variant = sys.argv[4] if len(sys.argv) > 4 else "wide"
 fn = btd.lib().btd_debug_timing_wide
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 32)()
 p = btdgen.dd(1, N, n, seed=1, device="cuda").cast(dt)
 btd.factor_solve(p.D, p.E, p.b, variant=variant)
 torch.cuda.synchronize()
@@ -29,3 +29,6 @@ tot = sum(buf[i] for i in range(8))
 for i, nm in enumerate(names):
     print(f"{nm:18s} {buf[i]:10d} cycles {buf[i] / max(tot, 1) * 100:5.1f}%")
 print("total", tot, "cycles (CTA 0)")
+if variant == "persist":
+    for i, nm in [(8, "  P1 diag blocks"), (9, "  P1 panel trsm"), (10, "  P1 trailing upd")]:
+        print(f"{nm:18s} {buf[i]:10d} cycles")
