@@ -100,13 +100,13 @@ def test_status_strings():
 
 
 def test_auto_rejects_oversized_persist_at_plan_time():
-    """n = 128 fp64 with many right-hand sides needs more than 227 KB of shared memory in PERSIST:
+    """n = 128 fp64 with 256 right-hand sides needs more than 227 KB of shared memory in PERSIST:
     AUTO refuses at plan creation (BTD_EUNSUPPORTED) instead of failing at every launch."""
     import ctypes
 
     L = btd.lib()
     h = ctypes.c_void_p()
-    assert L.btd_plan_create(ctypes.byref(h), 256, 128, 1, 64, 1) == 4
+    assert L.btd_plan_create(ctypes.byref(h), 256, 128, 1, 256, 1) == 4
     assert L.btd_plan_create(ctypes.byref(h), 256, 128, 1, 1, 1) == 0
     L.btd_plan_destroy(h)
 
