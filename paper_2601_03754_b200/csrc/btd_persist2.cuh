@@ -79,6 +79,24 @@ __device__ __forceinline__ void cta_load_block(T *S, int sld, const T *G, int gl
     __pipeline_wait_prior(0);
 }
 
+// cta_load_block without the commit/wait: several blocks share one commit group.
+template <typename T>
+__device__ __forceinline__ void cta_issue_block(T *S, int sld, const T *G, int gld, int rows, int cols) {
+    constexpr int W = 16 / (int)sizeof(T);
+    if (cols % W == 0 && gld % W == 0 && sld % W == 0 && (((uintptr_t)G) & 15) == 0) {
+        const int cw = cols / W;
+        for (int q = threadIdx.x; q < rows * cw; q += blockDim.x) {
+            const int i = q / cw, j = (q % cw) * W;
+            __pipeline_memcpy_async(S + (size_t)i * sld + j, G + (size_t)i * gld + j, 16);
+        }
+    } else {
+        for (int q = threadIdx.x; q < rows * cols; q += blockDim.x) {
+            const int i = q / cols, j = q % cols;
+            __pipeline_memcpy_async(S + (size_t)i * sld + j, G + (size_t)i * gld + j, sizeof(T));
+        }
+    }
+}
+
 // d += a * b over one m8n8k4 step (fp64 tensor core). Fragments (lane = 4 g + t): a = A[g][t],
 // b = B[t][g], d = {D[g][2t], D[g][2t+1]}.
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -90,10 +108,13 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 // One warp: C(8x8 at rows r0, cols c0 of S, ld lds) -= sum_{k<kb} P[r0+i][pk+k] Q[c0+j][pk+k], where P
 // and Q are row-major smem blocks (ld lds) -- the rank-kb update of a tile by a panel. Rows/cols
 // outside [0, rmax) / [0, cmax) are neither read nor written. T = double: DMMA; float: FFMA.
-template <typename T>
+// PT / QT: P / Q stored transposed (element (i, k) at P[k * ldp + i]).
+template <typename T, bool PT = false, bool QT = false>
 __device__ __forceinline__ void tile8_sub(T *S, int lds, int r0, int c0, int rmax, int cmax, const T *P, int ldp,
                                           const T *Q, int ldq, int pk, int kb) {
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    auto pel = [&](int i, int k) { return PT ? P[k * ldp + i] : P[i * ldp + k]; };
+    auto qel = [&](int j, int k) { return QT ? Q[k * ldq + j] : Q[j * ldq + k]; };
     if constexpr (sizeof(T) == 8) {
         double d[2];
         const int r = r0 + g, c = c0 + 2 * t;
@@ -102,8 +123,8 @@ __device__ __forceinline__ void tile8_sub(T *S, int lds, int r0, int c0, int rma
         const int pr = r0 + g, qr = c0 + g;
         for (int k = 0; k < kb; k += 4) {
             const int kk = pk + k + t;
-            const double a = (pr < rmax && k + t < kb) ? -P[pr * ldp + kk] : 0.0;
-            const double b = (qr < cmax && k + t < kb) ? Q[qr * ldq + kk] : 0.0;
+            const double a = (pr < rmax && k + t < kb) ? -pel(pr, kk) : 0.0;
+            const double b = (qr < cmax && k + t < kb) ? qel(qr, kk) : 0.0;
             dmma884(d, a, b);
         }
         if (r < rmax && c < cmax) S[r * lds + c] = d[0];
@@ -114,9 +135,9 @@ __device__ __forceinline__ void tile8_sub(T *S, int lds, int r0, int c0, int rma
         if (r >= rmax) return;
         T d0 = c < cmax ? S[r * lds + c] : T(0), d1 = c + 1 < cmax ? S[r * lds + c + 1] : T(0);
         for (int k = 0; k < kb; ++k) {
-            const T a = P[r * ldp + pk + k];
-            if (c < cmax) d0 = fma(-a, Q[c * ldq + pk + k], d0);
-            if (c + 1 < cmax) d1 = fma(-a, Q[(c + 1) * ldq + pk + k], d1);
+            const T a = pel(r, pk + k);
+            if (c < cmax) d0 = fma(-a, qel(c, pk + k), d0);
+            if (c + 1 < cmax) d1 = fma(-a, qel(c + 1, pk + k), d1);
         }
         if (c < cmax) S[r * lds + c] = d0;
         if (c + 1 < cmax) S[r * lds + c + 1] = d1;
@@ -142,7 +163,7 @@ __device__ __forceinline__ void pad_identity(T *A, int lda, int n, int np) {
 // sides stored transposed, zero-padded) carried through the panel TRSMs and trailing updates, so
 // that on return they hold (L^{-1} y)^T. dinv[k] = 1/L[k][k]; strict upper triangle of L set to zero.
 // Returns false if one of the first n pivots is <= 0 or NaN.
-template <typename T>
+template <typename T, int Q = kQ>
 __device__ bool cta_potrf_blocked(T *A, int lda, int n, int np, int ext, T *dinv) {
     __shared__ int s_ok;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -164,18 +185,18 @@ __device__ bool cta_potrf_blocked(T *A, int lda, int n, int np, int ext, T *dinv
     do {             \
     } while (0)
 #endif
-    for (int k0 = 0; k0 < np; k0 += kQ) {
-        const int k1 = k0 + kQ;
+    for (int k0 = 0; k0 < np; k0 += Q) {
+        const int k1 = k0 + Q;
         // (1) diagonal block, one warp: lane i owns row k0 + i; right-looking, shuffles
         if (warp == 0) {
-            T a[kQ];
+            T a[Q];
             const int i = lane;
 #pragma unroll
-            for (int j = 0; j < kQ; ++j) a[j] = (j <= i) ? A[(k0 + i) * lda + k0 + j] : T(0);
+            for (int j = 0; j < Q; ++j) a[j] = (i < Q && j <= i) ? A[(k0 + i) * lda + k0 + j] : ((i == j) ? T(1) : T(0));
             bool bad = false;
             T myinv = T(1);
 #pragma unroll
-            for (int k = 0; k < kQ; ++k) {
+            for (int k = 0; k < Q; ++k) {
                 const T akk = __shfl_sync(kFull, a[k], k);
                 bad |= (k0 + k < n) && !(akk > T(0));
                 T d, inv;
@@ -186,34 +207,36 @@ __device__ bool cta_potrf_blocked(T *A, int lda, int n, int np, int ext, T *dinv
                 // constant trip count (j > k becomes a compile-time predicate once unrolled): both
                 // loops must flatten or a[] is demoted to local memory
 #pragma unroll
-                for (int j = 1; j < kQ; ++j) {
+                for (int j = 1; j < Q; ++j) {
                     if (j <= k) continue;
                     const T ljk = __shfl_sync(kFull, a[k], j);
                     a[j] = fma(-a[k], ljk, a[j]);
                 }
             }
+            if (i < Q) {  // lanes >= Q (Q < 32) carry don't-care rows
 #pragma unroll
-            for (int j = 0; j < kQ; ++j)
-                if (j <= i) A[(k0 + i) * lda + k0 + j] = a[j];
-            dinv[k0 + i] = myinv;
+                for (int j = 0; j < Q; ++j)
+                    if (j <= i) A[(k0 + i) * lda + k0 + j] = a[j];
+                dinv[k0 + i] = myinv;
+            }
             if (bad && lane == 0) s_ok = 0;
         }
         __syncthreads();
         BTD_PSUB(8);
         // (2) panel TRSM: rows r >= k1 (and the ext rows): x <- x L11^{-T}, one thread per row
         for (int r = k1 + tid; r < rows; r += blockDim.x) {
-            T x[kQ];
+            T x[Q];
 #pragma unroll
-            for (int j = 0; j < kQ; ++j) x[j] = A[r * lda + k0 + j];
+            for (int j = 0; j < Q; ++j) x[j] = A[r * lda + k0 + j];
 #pragma unroll
-            for (int k = 0; k < kQ; ++k) {
+            for (int k = 0; k < Q; ++k) {
                 x[k] *= dinv[k0 + k];
 #pragma unroll
-                for (int j = 1; j < kQ; ++j)
+                for (int j = 1; j < Q; ++j)
                     if (j > k) x[j] = fma(-x[k], A[(k0 + j) * lda + k0 + k], x[j]);
             }
 #pragma unroll
-            for (int j = 0; j < kQ; ++j) A[r * lda + k0 + j] = x[j];
+            for (int j = 0; j < Q; ++j) A[r * lda + k0 + j] = x[j];
         }
         __syncthreads();
         BTD_PSUB(9);
@@ -228,13 +251,13 @@ __device__ bool cta_potrf_blocked(T *A, int lda, int n, int np, int ext, T *dinv
                     ++ti;
                 }
                 tile8_sub<T>(A + (size_t)k1 * lda + k1, lda, 8 * ti, 8 * q, np - k1, np - k1, A + (size_t)k1 * lda, lda,
-                             A + (size_t)k1 * lda, lda, k0, kQ);
+                             A + (size_t)k1 * lda, lda, k0, Q);
             }
             for (int q = tid; q < ext * (np - k1); q += blockDim.x) {
                 const int r = np + q / (np - k1), j = k1 + q % (np - k1);
                 T acc = A[r * lda + j];
 #pragma unroll 8
-                for (int k = 0; k < kQ; ++k) acc = fma(-A[r * lda + k0 + k], A[j * lda + k0 + k], acc);
+                for (int k = 0; k < Q; ++k) acc = fma(-A[r * lda + k0 + k], A[j * lda + k0 + k], acc);
                 A[r * lda + j] = acc;
             }
         }
@@ -252,24 +275,24 @@ __device__ bool cta_potrf_blocked(T *A, int lda, int n, int np, int ext, T *dinv
 // vector x <- L^{-1} x, CTA-wide. L: np x np lower (identity-padded) in smem, ld lda; dinv[k] =
 // 1/L[k][k]. Blocked: 32-column diagonal solves (one thread per vector), then the panel update of
 // the remaining columns on 8 x 8 tiles (DMMA for fp64).
-template <typename T>
+template <typename T, int Q = kQ>
 __device__ void cta_trsm_blocked(T *X, int ldx, int nv, const T *L, int lda, int np, const T *dinv) {
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int k0 = 0; k0 < np; k0 += kQ) {
-        const int k1 = k0 + kQ;
+    for (int k0 = 0; k0 < np; k0 += Q) {
+        const int k1 = k0 + Q;
         for (int v = tid; v < nv; v += blockDim.x) {
-            T x[kQ];
+            T x[Q];
 #pragma unroll
-            for (int j = 0; j < kQ; ++j) x[j] = X[v * ldx + k0 + j];
+            for (int j = 0; j < Q; ++j) x[j] = X[v * ldx + k0 + j];
 #pragma unroll
-            for (int k = 0; k < kQ; ++k) {
+            for (int k = 0; k < Q; ++k) {
                 x[k] *= dinv[k0 + k];
 #pragma unroll
-                for (int j = 1; j < kQ; ++j)
+                for (int j = 1; j < Q; ++j)
                     if (j > k) x[j] = fma(-x[k], L[(k0 + j) * lda + k0 + k], x[j]);
             }
 #pragma unroll
-            for (int j = 0; j < kQ; ++j) X[v * ldx + k0 + j] = x[j];
+            for (int j = 0; j < Q; ++j) X[v * ldx + k0 + j] = x[j];
         }
         __syncthreads();
         if (k1 < np) {
@@ -277,7 +300,7 @@ __device__ void cta_trsm_blocked(T *X, int ldx, int nv, const T *L, int lda, int
             const int tr = (nv + 7) / 8, tc = (np - k1) / 8;
             for (int tt = warp; tt < tr * tc; tt += blockDim.x / 32) {
                 const int ti = tt / tc, tj = tt % tc;
-                tile8_sub<T>(X + k1, ldx, 8 * ti, 8 * tj, nv, np - k1, X, ldx, L + (size_t)k1 * lda, lda, k0, kQ);
+                tile8_sub<T>(X + k1, ldx, 8 * ti, 8 * tj, nv, np - k1, X, ldx, L + (size_t)k1 * lda, lda, k0, Q);
             }
         }
         __syncthreads();

@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include "btd_kernels.cuh"
+#include "btd_persist2.cuh"
 
 namespace btd {
 
@@ -37,8 +38,12 @@ template <typename T>
 struct WideSmem {
     static __host__ __device__ int nb(int n) { return n <= 8 ? 8 : n <= 16 ? 16 : 32; }
     static __host__ __device__ size_t elems(int n, int m) {
+        // forward task: A (+ m y rows), Cr, ClT, Cd, Ce, Sep, F with ld NB+4; ys, yt, yu; dinv
+        const size_t fwd = (size_t)(7 * nb(n) + m) * (nb(n) + 4) + 3 * (size_t)n * m + nb(n);
+        // backward task (ld NB+1)
         const size_t blk = (size_t)nb(n) * (nb(n) + 1);
-        return 7 * blk + 6 * (size_t)n * m + 2 * (size_t)nb(n) + 32;
+        const size_t bwd = 4 * blk + 3 * (size_t)n * m + nb(n);
+        return (fwd > bwd ? fwd : bwd) + 32;
     }
     static __host__ __device__ size_t bytes(int n, int m) { return elems(n, m) * sizeof(T); }
 };
@@ -339,6 +344,189 @@ __device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int3
     BTD_STAMP(4);
 }
 
+
+// One column op of level l (Alg. 4 l.7-l.13 + Alg. 6 forward) by one CTA, built from the blocked
+// PERSIST2 pieces at panel width NB: blocks staged with 16-byte copies (ld NB+4, identity/zero
+// padded to NB), the deferred downdates (l.7, l.9), l.11 and the fill (l.13) as 8 x 8 tiles (DMMA
+// for fp64), the POTRF by one warp with the y rows riding along (Alg. 6 l.4), both TRSMs as one
+// batch of 2 NB vectors (rows of C_r, columns of C_l).
+template <typename T, int NB>
+__device__ void wide_fwd_task2(const T *__restrict__ E, T *Dhat, T *C, T *x, int32_t *info, const Geo &g, int l,
+                               long long sys, int j, bool fact, bool solve, T *sm
+#ifdef BTD_TIMING
+                               , unsigned long long &btd_t_last
+#endif
+) {
+    const int N = g.N, n = g.n, m = g.m;
+    constexpr int LDW = NB + 4;
+    constexpr size_t BLK = (size_t)NB * LDW;
+    const size_t nn = (size_t)n * n;
+    const int s = 1 << (l - 1);
+    const int c = s * (2 * j + 1);
+    const bool hasL = c > s, hasR = c + s <= N;
+    const bool defC = l > 1 && (c + s / 2 <= N);
+    const bool defS = l > 1 && (c + s + s / 2 <= N);
+    const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
+    T *Dh = Dhat + sys * N * nn;
+    T *Cs = C + sys * (size_t)g.nC * nn;
+    T *xs = x ? x + sys * (size_t)N * n * m : nullptr;
+    const int ext = solve ? m : 0;
+    T *A = sm;                                  // (NB + ext) x LDW: D~_c, then L; rows NB..: y_c^T
+    T *Cr = A + (size_t)(NB + ext) * LDW;       // rows of C_r
+    T *ClT = Cr + BLK;                          // columns of C_l as rows (must follow Cr)
+    T *Cd = ClT + BLK, *Ce = Cd + BLK, *Sep = Ce + BLK, *F = Sep + BLK;
+    T *ys = F + BLK, *yt = ys + (size_t)n * m, *yu = yt + (size_t)n * m;
+    T *dinv = yu + (size_t)n * m;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    const long long sR = cslot(g, l, c / s), sL = cslot(g, l, hasL ? c / s - 1 : 1);
+    const T *CrSrc = l == 1 ? Es + (size_t)(c - 1) * nn : Cs + sR * nn;
+    const T *ClSrc = l == 1 ? Es + (size_t)(c - 2) * nn : Cs + sL * nn;
+
+    // ---- one round of loads (LDGSTS) + padding
+    cta_issue_block<T>(A, LDW, Dh + (size_t)(c - 1) * nn, n, n, n);
+    if (fact && hasR) {
+        cta_issue_block<T>(Cr, LDW, CrSrc, n, n, n);
+        cta_issue_block<T>(Sep, LDW, Dh + (size_t)(c + s - 1) * nn, n, n, n);
+    }
+    if (!fact && hasR) cta_issue_block<T>(Cr, LDW, Cs + sR * nn, n, n, n);
+    if (defC) cta_issue_block<T>(Cd, LDW, Cs + cslot(g, l - 1, 2 * c / s) * nn, n, n, n);
+    if (defS) cta_issue_block<T>(Ce, LDW, Cs + cslot(g, l - 1, 2 * c / s + 2) * nn, n, n, n);
+    __pipeline_commit();
+    if (fact && hasL)  // columns of C_l, transposed (lanes over the contiguous index)
+        for (int i = warp; i < n; i += nw)
+            for (int v = lane; v < n; v += 32) ClT[v * LDW + i] = ClSrc[(size_t)i * n + v];
+    if (solve) {
+        for (int q = tid; q < n * m; q += blockDim.x) {
+            const int i = q / m, r = q % m;
+            A[(NB + r) * LDW + i] = xs[(size_t)(c - 1) * n * m + q];
+            if (defC) ys[q] = xs[(size_t)(c + s / 2 - 1) * n * m + q];
+            if (hasR) yt[q] = xs[(size_t)(c + s - 1) * n * m + q];
+            if (defS) yu[q] = xs[(size_t)(c + s + s / 2 - 1) * n * m + q];
+        }
+        for (int q = tid; q < m * (NB - n); q += blockDim.x) A[(NB + q / (NB - n)) * LDW + n + q % (NB - n)] = T(0);
+    }
+    // padding: A identity, the other blocks zero, outside the leading n x n
+    if (n < NB) {
+        for (int q = tid; q < NB * NB; q += blockDim.x) {
+            const int i = q / NB, jj = q % NB;
+            if (i >= n || jj >= n) {
+                A[i * LDW + jj] = (i == jj) ? T(1) : T(0);
+                Cr[i * LDW + jj] = T(0);
+                ClT[i * LDW + jj] = T(0);
+            }
+        }
+    }
+    if (fact && !hasR)
+        for (int q = tid; q < NB * NB; q += blockDim.x) Cr[(q / NB) * LDW + q % NB] = T(0);
+    if (fact && !hasL)
+        for (int q = tid; q < NB * NB; q += blockDim.x) ClT[(q / NB) * LDW + q % NB] = T(0);
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    BTD_STAMP(0);
+    const int nt = (n + 7) / 8, ntri = nt * (nt + 1) / 2;
+    // ---- l.7 / l.9 deferred left downdates  A -= Cd^T Cd,  Sep -= Ce^T Ce  (lower 8 x 8 tiles)
+    if (fact && (defC || defS)) {
+        for (int tt = warp; tt < 2 * ntri; tt += nw) {
+            const bool second = tt >= ntri;
+            if (second ? !defS : !defC) continue;
+            int ti = 0, q = second ? tt - ntri : tt;
+            while (q > ti) {
+                q -= ti + 1;
+                ++ti;
+            }
+            const T *M = second ? Ce : Cd;
+            tile8_sub<T, true, true>(second ? Sep : A, LDW, 8 * ti, 8 * q, n, n, M, LDW, M, LDW, 0, n);
+        }
+    }
+    if (solve && (defC || defS)) {  // y_c -= Cd^T y_{c+s/2} ;  y_{c+s} -= Ce^T y_{c+3s/2}
+        for (int q = tid; q < 2 * n * m; q += blockDim.x) {
+            const bool second = q >= n * m;
+            if (second ? !defS : !defC) continue;
+            const int qq = second ? q - n * m : q, i = qq / m, r = qq % m;
+            const T *M = second ? Ce : Cd;
+            const T *src = second ? yu : ys;
+            T acc = T(0);
+            for (int k = 0; k < n; ++k) acc = fma(M[k * LDW + i], src[k * m + r], acc);
+            if (second)
+                yt[qq] -= acc;
+            else
+                A[(NB + r) * LDW + i] -= acc;
+        }
+    }
+    __syncthreads();
+    BTD_STAMP(1);
+    // ---- l.8 POTRF + Alg. 6 l.4 (the y rows)
+    if (fact) {
+        const bool ok = cta_potrf_blocked<T, NB>(A, LDW, n, NB, ext, dinv);
+        if (!ok && tid == 0) report_fail(info + sys, c);
+    } else {
+        for (int i = tid; i < NB; i += blockDim.x) dinv[i] = T(1) / A[i * LDW + i];
+        __syncthreads();
+        if (ext) cta_trsm_blocked<T, NB>(A + (size_t)NB * LDW, LDW, ext, A, LDW, NB, dinv);
+    }
+    BTD_STAMP(2);
+    // ---- l.10 / l.12 TRSMs: rows of C_r and columns of C_l, one batch of 2 NB vectors
+    if (fact) cta_trsm_blocked<T, NB>(Cr, LDW, 2 * NB, A, LDW, NB, dinv);
+    BTD_STAMP(3);
+    // ---- stores of this column's L^ blocks and y_c
+    if (fact) {
+        T *dst = Dh + (size_t)(c - 1) * nn;
+        for (int i = warp; i < n; i += nw)
+            for (int jj = lane; jj < n; jj += 32) dst[(size_t)i * n + jj] = A[i * LDW + jj];
+        if (hasR) {
+            T *d2 = Cs + sR * nn;
+            for (int i = warp; i < n; i += nw)
+                for (int jj = lane; jj < n; jj += 32) d2[(size_t)i * n + jj] = Cr[i * LDW + jj];
+        }
+        if (hasL) {
+            T *d2 = Cs + sL * nn;
+            for (int i = warp; i < n; i += nw)
+                for (int v = lane; v < n; v += 32) d2[(size_t)i * n + v] = ClT[v * LDW + i];
+        }
+    }
+    if (solve)
+        for (int q = tid; q < n * m; q += blockDim.x) xs[(size_t)(c - 1) * n * m + q] = A[(NB + q % m) * LDW + q / m];
+    // ---- l.11 right downdate  Sep -= Cr Cr^T  and l.13 fill  F = -Cr Cl  (8 x 8 tiles)
+    if (fact && hasR) {
+        const bool fill = hasL && hasR;
+        if (fill)
+            for (int q = tid; q < NB * NB; q += blockDim.x) F[(q / NB) * LDW + q % NB] = T(0);
+        __syncthreads();
+        for (int tt = warp; tt < ntri + (fill ? nt * nt : 0); tt += nw) {
+            if (tt < ntri) {
+                int ti = 0, q = tt;
+                while (q > ti) {
+                    q -= ti + 1;
+                    ++ti;
+                }
+                tile8_sub<T>(Sep, LDW, 8 * ti, 8 * q, n, n, Cr, LDW, Cr, LDW, 0, n);
+            } else {
+                const int t2 = tt - ntri;
+                tile8_sub<T>(F, LDW, 8 * (t2 / nt), 8 * (t2 % nt), n, n, Cr, LDW, ClT, LDW, 0, n);
+            }
+        }
+        __syncthreads();
+        T *dsep = Dh + (size_t)(c + s - 1) * nn;
+        for (int i = warp; i < n; i += nw)
+            for (int jj = lane; jj < n; jj += 32) dsep[(size_t)i * n + jj] = Sep[i * LDW + jj];
+        if (fill) {
+            T *dF = Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn;
+            for (int i = warp; i < n; i += nw)
+                for (int jj = lane; jj < n; jj += 32) dF[(size_t)i * n + jj] = F[i * LDW + jj];
+        }
+    }
+    if (solve && hasR) {  // y_{c+s} = yt - C_r y_c
+        for (int q = tid; q < n * m; q += blockDim.x) {
+            const int i = q / m, r = q % m;
+            T acc = T(0);
+            for (int k = 0; k < n; ++k) acc = fma(Cr[i * LDW + k], A[(NB + r) * LDW + k], acc);
+            xs[(size_t)(c + s - 1) * n * m + q] = yt[q] - acc;
+        }
+    }
+    __syncthreads();
+    BTD_STAMP(4);
+}
+
 template <typename T, int NB>
 __device__ void wide_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int l, long long sys, int j, T *sm) {
     const int N = g.N, n = g.n, m = g.m;
@@ -410,7 +598,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
     for (int l = 1; l <= g.L; ++l) {
         const int ncols = ((g.N >> (l - 1)) + 1) / 2;
         for (long long task = blockIdx.x; task < (long long)batch * ncols; task += gridDim.x)
-            wide_fwd_task<T, NB>(E, Dhat, C, x, info, g, l, task / ncols, (int)(task % ncols), fact, solve, sm
+            wide_fwd_task2<T, NB>(E, Dhat, C, x, info, g, l, task / ncols, (int)(task % ncols), fact, solve, sm
 #ifdef BTD_TIMING
                                  , btd_t_last
 #endif
