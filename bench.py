@@ -237,12 +237,12 @@ def _l2_flusher(dev):
     return lambda: buf.fill_(1.0)
 
 
-def _latency_case(dev, s, N, n, dt, reps, flush):
+def _latency_case(dev, s, N, n, dt, reps, flush, variant="auto"):
     import btdgen
     import paper_2601_03754_b200 as btd
 
     p = btdgen.kalman(1, N, n, seed=N, device=dev).cast(dt)
-    plan = btd.Plan(N, n, 1, 1, dt)
+    plan = btd.Plan(N, n, 1, 1, dt, variant)
     outs = (torch.empty_like(p.D), torch.empty(1, plan.num_coupling_blocks, n, n, dtype=dt, device=dev),
             torch.empty_like(p.b), torch.empty(1, dtype=torch.int32, device=dev))
 
@@ -287,7 +287,11 @@ def _latency_sweep(dev) -> dict:
     cases = [("c1_fp64_n2", 2, torch.float64, [8]), ("c2_fp64_n16", 16, torch.float64, [64]),
              ("c3_fp64_n32", 32, torch.float64, [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]),
              ("c3_fp32_n32", 32, torch.float32, [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]),
-             ("c4_fp64_n128", 128, torch.float64, [256])]
+             ("c4_fp64_n128", 128, torch.float64, [256]),
+             # Alg. 5 (right-looking, atomic Schur updates) against the deferred schedule (§8(f) f2)
+             ("c2_fp64_n16_atomic", 16, torch.float64, [64]),
+             ("c3_fp64_n32_atomic", 32, torch.float64, [64, 256, 1024]),
+             ("c3_fp32_n32_atomic", 32, torch.float32, [64, 256, 1024])]
     # n-sweep at N = 512, fp64 (the paper's block-size experiment)
     nsweep = [("nsweep_fp64_N512_n%d" % n, n, torch.float64, [512]) for n in (4, 8, 12, 16, 24, 32, 48, 64, 96)]
     s = torch.cuda.Stream(dev)
@@ -296,7 +300,8 @@ def _latency_sweep(dev) -> dict:
         res = {}
         w = 8 if dt == torch.float64 else 4
         for N in Ns:
-            r = _latency_case(dev, s, N, n, dt, 50 if n <= 32 else 5, flush)
+            r = _latency_case(dev, s, N, n, dt, 50 if n <= 32 else 5, flush,
+                              "atomic" if name.endswith("_atomic") else "auto")
             fl = algorithmic_flops_per_system(N, n, 1)
             by = algorithmic_bytes_per_system(N, n, 1, w)["total"]
             t_fp = fl / ((pk["fp64_tflops"] if w == 8 else pk["fp32_tflops"]) * 1e12) * 1e6

@@ -81,7 +81,12 @@ typedef enum {
     BTD_VARIANT_FUSED = 1, /* one CTA per system, all levels + both sweeps in one launch, state in smem */
     BTD_VARIANT_LEVEL = 2, /* one launch per level (Alg. 4 deferred form), state in the output buffers */
     BTD_VARIANT_PERSIST = 3, /* one cooperative launch, all levels as grid-wide phases; any n <= 128 */
-    BTD_VARIANT_WIDE = 4     /* one cooperative launch, one CTA per column op (single systems, n <= 32) */
+    BTD_VARIANT_WIDE = 4,    /* one cooperative launch, one CTA per column op (single systems, n <= 32) */
+    BTD_VARIANT_ATOMIC = 5   /* WIDE with Algorithm 5's schedule: fully right-looking,
+                                both Schur updates of a column pushed with atomic adds (contention <= 2,
+                                P:660), per-level chain potrf -> trsm -> syrk; n <= 32. The summation
+                                order at a separator is not deterministic: results agree with the other
+                                variants to rounding, not bitwise. */
 } btd_variant;
 
 /* Create a plan for `batch` systems of N blocks of size n with m right-hand sides.
@@ -102,7 +107,7 @@ int64_t btd_num_coupling_blocks(const btd_plan *plan);
 int64_t btd_level_offset(const btd_plan *plan, int32_t level);
 /* P_inf as host array perm[new position] = original index, both 0-based. */
 btd_status btd_permutation(const btd_plan *plan, int64_t *host_perm);
-/* The variant the plan will launch (BTD_VARIANT_FUSED, _LEVEL, _PERSIST or _WIDE). */
+/* The variant the plan will launch (BTD_VARIANT_FUSED, _LEVEL, _PERSIST, _WIDE or _ATOMIC). */
 int32_t btd_plan_variant(const btd_plan *plan);
 /* Number of kernel launches one call of factor / solve / factor_solve makes (op = 0 / 1 / 2). */
 int32_t btd_plan_launches(const btd_plan *plan, int32_t op);

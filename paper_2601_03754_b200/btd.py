@@ -20,8 +20,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BTD_LIB") or os.path.join(_HERE, "libbtd.so")  # BTD_LIB: dev override (timing build)
 
 BTD_F32, BTD_F64 = 0, 1
-VARIANTS = {"auto": 0, "fused": 1, "level": 2, "persist": 3, "wide": 4}
-VARIANT_NAMES = {1: "fused", 2: "level", 3: "persist", 4: "wide"}
+VARIANTS = {"auto": 0, "fused": 1, "level": 2, "persist": 3, "wide": 4, "atomic": 5}
+VARIANT_NAMES = {1: "fused", 2: "level", 3: "persist", 4: "wide", 5: "atomic"}
 _STATUS = {0: "BTD_OK", 1: "BTD_EINVAL", 2: "BTD_ECUDA", 3: "BTD_ENOMEM", 4: "BTD_EUNSUPPORTED"}
 
 _lib = None

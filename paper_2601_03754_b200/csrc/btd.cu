@@ -88,7 +88,7 @@ static size_t fused_bytes_dt(const btd_plan *p, bool fact, bool solve) {
 static btd_status run(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
                       void *x, int32_t *info, int64_t sys0, int64_t count, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (p->variant == BTD_VARIANT_WIDE) {
+    if (p->variant == BTD_VARIANT_WIDE || p->variant == BTD_VARIANT_ATOMIC) {
         if (p->dtype == BTD_F32) return run_wide<float>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
         return run_wide<double>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
     }
@@ -143,9 +143,10 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
     if (N < 1 || n < 1 || batch < 1 || m < 1 || (dtype != BTD_F32 && dtype != BTD_F64)) return BTD_EINVAL;
     if (N > (1ll << 24) || m > 4096) return BTD_EINVAL;
     if (n > 128) return BTD_EUNSUPPORTED;
-    if (variant < BTD_VARIANT_AUTO || variant > BTD_VARIANT_WIDE) return BTD_EINVAL;
+    if (variant < BTD_VARIANT_AUTO || variant > BTD_VARIANT_ATOMIC) return BTD_EINVAL;
     const int NB = pick_nb(n);  // -1 for n > 32: only PERSIST handles those
-    if (NB < 0 && (variant == BTD_VARIANT_FUSED || variant == BTD_VARIANT_LEVEL || variant == BTD_VARIANT_WIDE))
+    if (NB < 0 && (variant == BTD_VARIANT_FUSED || variant == BTD_VARIANT_LEVEL || variant == BTD_VARIANT_WIDE ||
+                   variant == BTD_VARIANT_ATOMIC))
         return BTD_EUNSUPPORTED;
     btd_plan *p = new (std::nothrow) btd_plan();
     if (!p) return BTD_ENOMEM;
@@ -187,7 +188,7 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         return BTD_EUNSUPPORTED;
     }
     const size_t wsm = f32 ? WideSmem<float>::bytes((int)n, (int)m) : WideSmem<double>::bytes((int)n, (int)m);
-    if (variant == BTD_VARIANT_WIDE && wsm > kMaxSmem) {
+    if ((variant == BTD_VARIANT_WIDE || variant == BTD_VARIANT_ATOMIC) && wsm > kMaxSmem) {
         delete p;
         return BTD_EUNSUPPORTED;
     }

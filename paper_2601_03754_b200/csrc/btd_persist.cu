@@ -76,12 +76,12 @@ btd_status run_persist(const btd_plan *p, int op, const void *D, const void *E, 
     return BTD_OK;
 }
 
-template <typename T, int NB>
+template <typename T, int NB, bool ATOMIC>
 static btd_status launch_wide(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat,
                               void *C, void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
     const int n = (int)p->n, m = (int)p->m, N = (int)p->N;
     const size_t smem = WideSmem<T>::bytes(n, m);
-    auto kern = btd_wide_kernel<T, NB>;
+    auto kern = btd_wide_kernel<T, NB, ATOMIC>;
     if (btd_status rs = ensure_smem_attr((const void *)kern, smem); rs != BTD_OK) return rs;
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
@@ -112,9 +112,14 @@ static btd_status launch_wide(const btd_plan *p, int op, const void *D, const vo
 template <typename T>
 btd_status run_wide(const btd_plan *p, int op, const void *D, const void *E, const void *b, void *Dhat, void *C,
                     void *x, int32_t *info, int64_t sys0, int64_t count, cudaStream_t st) {
-    if (p->n <= 8) return launch_wide<T, 8>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
-    if (p->n <= 16) return launch_wide<T, 16>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
-    return launch_wide<T, 32>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    if (p->variant == BTD_VARIANT_ATOMIC) {
+        if (p->n <= 8) return launch_wide<T, 8, true>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+        if (p->n <= 16) return launch_wide<T, 16, true>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+        return launch_wide<T, 32, true>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    }
+    if (p->n <= 8) return launch_wide<T, 8, false>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    if (p->n <= 16) return launch_wide<T, 16, false>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
+    return launch_wide<T, 32, false>(p, op, D, E, b, Dhat, C, x, info, sys0, count, st);
 }
 
 template btd_status run_wide<float>(const btd_plan *, int, const void *, const void *, const void *, void *, void *,

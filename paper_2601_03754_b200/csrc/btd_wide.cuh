@@ -4,21 +4,21 @@
 // grid-wide phase in which every column op is executed by a whole CTA (256 threads), and levels
 // are separated by grid.sync(). Compared with one warp per column op (LEVEL / PERSIST-TEAM) this
 // shortens the per-level critical path -- the quantity that sets single-system latency once the
-// first levels no longer fill the GPU -- to: one round of loads, the deferred
-// downdate GEMM, one warp's POTRF, one TRSM per vector (64 vectors in parallel), the downdate and
-// fill GEMMs spread over the CTA. All loops are rolled (n is a runtime value): the kernel's code
-// stays resident in the instruction cache, which the single-warp unrolled variants thrash.
+// first levels no longer fill the GPU.
 //
-// Per column c of level l (stride s), with every block staged in shared memory (ld n+1):
+// Per column c of level l (stride s), every block staged in shared memory (ld NB+4, padded to
+// NB in {8, 16, 32} with an identity diagonal / zeros), wide_fwd_task2:
 //   l.7   A   = D~_c   - Cd^T Cd        Cd = E^_{l-1,2c/s}   (stored left coupling of column c+s/2)
 //   l.9   Sep = D~_c+s - Ce^T Ce        Ce = E^_{l-1,2c/s+2} (stored left coupling of column c+3s/2)
-//   l.8   A   = chol(A)                 -> Dhat[c]
+//   l.8   A   = chol(A)                 -> Dhat[c]     (one warp; y_c rides along, Alg. 6 l.4)
 //   l.10  Cr  = Cr A^-T                 -> C[slot(l, c/s)]
 //   l.12  Cl  = A^-1 Cl                 -> C[slot(l, c/s-1)]
 //   l.11  Sep -= Cr Cr^T                -> Dhat[c+s]
 //   l.13  C[slot(l+1,(c-s)/2s)] = -Cr Cl
 //   Alg. 6 forward: y_c -= Cd^T y_{c+s/2}; y_c = A^-1 y_c; y_{c+s} -= Ce^T y_{c+3s/2} + Cr y_c
-// and the backward sweep: x_c = A^-T (y_c - Cr^T x_{c+s} - Cl x_{c-s}) one CTA per column.
+// with the Schur/fill products on 8 x 8 tiles (DMMA for fp64), and the backward sweep
+// x_c = A^-T (y_c - Cr^T x_{c+s} - Cl x_{c-s}) one CTA per column. The ATOMIC instantiation is
+// Algorithm 5 (right-looking, atomic Schur updates; variant BTD_VARIANT_ATOMIC).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -29,9 +29,8 @@ namespace btd {
 
 constexpr int kWThreads = 256;
 
-// Blocks are staged with a compile-time leading dimension NB+1 (NB in {8,16,32} >= n): every
-// address inside the rolled loops is base + immediate, and the +1 keeps column walks conflict-free.
-// A guard block at the end absorbs the look-ahead reads past row n of the last block.
+// Backward-task blocks are staged with a compile-time leading dimension NB+1 (NB in {8,16,32}
+// >= n): the +1 keeps column walks conflict-free.
 template <int n_>
 constexpr int wide_nb() { return n_ <= 8 ? 8 : n_ <= 16 ? 16 : 32; }
 template <typename T>
@@ -48,103 +47,16 @@ struct WideSmem {
     static __host__ __device__ size_t bytes(int n, int m) { return elems(n, m) * sizeof(T); }
 };
 
-// Cholesky of the n x n block A (ld lda, lower read) by ONE warp: lane r keeps row r of the
-// trailing matrix in a register window whose slot 0 is always the current column, so the column
-// loop is rolled while the register indices stay compile-time. Column k of L is published in A
-// (shared memory) and read back as broadcasts. The forward substitution of the m right-hand
-// sides y (n x m, shared memory) rides along (Alg. 6 l.4 interlaced with l.8). Writes L (lower;
-// strict upper 0) to A and 1/L[k][k] to dinv. Returns the first failing pivot or -1.
-template <typename T, int NB>
-__device__ int warp_potrf_rot(T *A, int n, T *dinv, T *y, int m) {
-    constexpr int LD = NB + 1;
-    const int r = threadIdx.x & 31;
-    T a[NB];
-#pragma unroll
-    for (int j = 0; j < NB; ++j) a[j] = (r < n && j < n) ? A[r * LD + j] : T(0);
-    int bad = -1;
-    for (int k = 0; k < n; ++k) {
-        const T akk = __shfl_sync(kFull, a[0], k);
-        bad = (!(akk > T(0)) && bad < 0) ? k : bad;
-        T d, inv;
-        pivot(akk, d, inv);
-        const T a0 = (r == k) ? d : a[0] * inv;  // L[r][k] for r >= k
-        if (r >= k && r < n) A[r * LD + k] = a0;
-        if (r == 0) dinv[k] = inv;
-        if (y && r == k)
-            for (int q = 0; q < m; ++q) y[k * m + q] *= inv;
-        __syncwarp();
-        const T *col = A + k * (LD + 1);  // col[jj * LD] = L[k+jj][k]; rows >= n are don't-care
-#pragma unroll
-        for (int jj = 1; jj < NB; ++jj) a[jj - 1] = fma(-a0, col[jj * LD], a[jj]);
-        a[NB - 1] = T(0);
-        if (y && r > k && r < n)
-            for (int q = 0; q < m; ++q) y[r * m + q] = fma(-a0, y[k * m + q], y[r * m + q]);
-        __syncwarp();
-    }
-    for (int q = r; q < n * n; q += 32) {
-        const int i = q / n, j = q % n;
-        if (j > i) A[i * LD + j] = T(0);
-    }
-    return bad;
-}
-
-// Quad of lanes (4 consecutive) solves L x = b for one vector stored in shared memory with stride
-// xs (x[i*xs]); left-looking, the dot products split over the quad and reduced by shuffles.
-template <typename T>
-__device__ void quad_trsv_lower(const T *L, int lda, const T *dinv, int n, T *x, int xs, bool active) {
-    const int q = threadIdx.x & 3;
-    for (int i = 0; i < n; ++i) {
-        T acc = T(0);
-        if (active)
-            for (int k = q; k < i; k += 4) acc = fma(L[i * lda + k], x[k * xs], acc);
-        acc += __shfl_xor_sync(kFull, acc, 1);
-        acc += __shfl_xor_sync(kFull, acc, 2);
-        if (active && q == 0) x[i * xs] = (x[i * xs] - acc) * dinv[i];
-        __syncwarp();
-    }
-}
-
-// One thread: x <- L^{-1} x for a vector of length n <= NB in registers (rotating window),
-// L lower in shared memory (ld NB+1), dinv the reciprocal diagonal; result to out[i*ostride].
-template <typename T, int NB>
-__device__ void thread_trsv_lower(T (&x)[NB], const T *L, const T *dinv, int n, T *out, int ostride) {
-    constexpr int LD = NB + 1;
-    for (int k = 0; k < n; ++k) {
-        const T xk = x[0] * dinv[k];
-        out[(size_t)k * ostride] = xk;
-        const T *col = L + k * (LD + 1);
-#pragma unroll
-        for (int jj = 1; jj < NB; ++jj) x[jj - 1] = fma(-xk, col[jj * LD], x[jj]);
-        x[NB - 1] = T(0);
-    }
-}
-
-// Fully unrolled variants (compile-time NB): the compiler hoists every shared-memory load far
-// ahead of its use, which the rolled rotating-window loop cannot do (3-4x faster measured, see
-// tools/micro/trsv_variants.cu).
-template <typename T, int NB>
-__device__ __forceinline__ void thread_trsv_unrolled(T (&x)[NB], const T *L, const T *dinv, int n, T *out,
-                                                     int ostride) {
-    constexpr int LD = NB + 1;
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-        if (k < n) {  // padding rows/columns of L and dinv are never read (may hold stale data)
-            x[k] *= dinv[k];
-            out[(size_t)k * ostride] = x[k];
-#pragma unroll
-            for (int j = k + 1; j < NB; ++j) x[j] = fma(-x[k], L[j * LD + k], x[j]);
-        }
-    }
-}
-
-// x <- L^{-T} x (back substitution), same conventions.
+// One thread: x <- L^{-T} x (back substitution) for a vector of length n <= NB in registers, L lower
+// in shared memory (ld NB+1), dinv the reciprocal diagonal; result to out[i*ostride]. Fully
+// unrolled: the compiler hoists the shared-memory loads ahead of their uses.
 template <typename T, int NB>
 __device__ __forceinline__ void thread_trsv_upper_t(T (&x)[NB], const T *L, const T *dinv, int n, T *out,
                                                     int ostride) {
     constexpr int LD = NB + 1;
 #pragma unroll
     for (int k = NB - 1; k >= 0; --k) {
-        if (k < n) {  // see thread_trsv_unrolled: padding never read
+        if (k < n) {  // padding rows/columns of L and dinv are never read
             x[k] *= dinv[k];
             out[(size_t)k * ostride] = x[k];
 #pragma unroll
@@ -161,196 +73,17 @@ __device__ __forceinline__ void wide_copy_block(T *dst, int ldd, const T *src, i
         __pipeline_memcpy_async(dst + (q / n) * ldd + (q % n), src + q, sizeof(T));
 }
 
-template <typename T, int NB>
-__device__ void wide_fwd_task(const T *__restrict__ E, T *Dhat, T *C, T *x, int32_t *info, const Geo &g, int l,
-                              long long sys, int j, bool fact, bool solve, T *sm
-#ifdef BTD_TIMING
-                              , unsigned long long &btd_t_last
-#endif
-) {
-    const int N = g.N, n = g.n, m = g.m;
-    constexpr int lda = NB + 1;
-    const size_t nn = (size_t)n * n, blk = (size_t)NB * lda;
-    const int s = 1 << (l - 1);
-    const int c = s * (2 * j + 1);
-    const bool hasL = c > s, hasR = c + s <= N;
-    const bool defC = l > 1 && (c + s / 2 <= N);
-    const bool defS = l > 1 && (c + s + s / 2 <= N);
-    const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
-    T *Dh = Dhat + sys * N * nn;
-    T *Cs = C + sys * (size_t)g.nC * nn;
-    T *xs = x ? x + sys * (size_t)N * n * m : nullptr;
-    T *A = sm, *Cr = A + blk, *Cl = Cr + blk, *Cd = Cl + blk, *Ce = Cd + blk, *Sep = Ce + blk;
-    T *yc = Sep + 2 * blk, *ys = yc + (size_t)n * m, *yt = ys + (size_t)n * m, *yu = yt + (size_t)n * m;  // Sep + guard
-    T *dinv = yu + (size_t)n * m;
-    __shared__ int s_bad;
-    const int tid = threadIdx.x, warp = tid >> 5;
-
-    // ---- one round of loads
-    const long long sR = cslot(g, l, c / s), sL = cslot(g, l, hasL ? c / s - 1 : 1);
-    wide_copy_block(A, lda, Dh + (size_t)(c - 1) * nn, n);
-    if (fact) {
-        if (hasR) wide_copy_block(Cr, lda, l == 1 ? Es + (size_t)(c - 1) * nn : Cs + sR * nn, n);
-        if (hasL) wide_copy_block(Cl, lda, l == 1 ? Es + (size_t)(c - 2) * nn : Cs + sL * nn, n);
-        if (hasR) wide_copy_block(Sep, lda, Dh + (size_t)(c + s - 1) * nn, n);
-    } else {
-        if (hasR) wide_copy_block(Cr, lda, Cs + sR * nn, n);
-    }
-    if (defC) wide_copy_block(Cd, lda, Cs + cslot(g, l - 1, 2 * c / s) * nn, n);
-    if (defS) wide_copy_block(Ce, lda, Cs + cslot(g, l - 1, 2 * c / s + 2) * nn, n);
-    if (solve) {
-        for (int q = tid; q < n * m; q += blockDim.x) {
-            yc[q] = xs[(size_t)(c - 1) * n * m + q];
-            if (defC) ys[q] = xs[(size_t)(c + s / 2 - 1) * n * m + q];
-            if (hasR) yt[q] = xs[(size_t)(c + s - 1) * n * m + q];
-            if (defS) yu[q] = xs[(size_t)(c + s + s / 2 - 1) * n * m + q];
-        }
-    }
-    if (tid == 0) s_bad = -1;
-    __pipeline_commit();
-    __pipeline_wait_prior(0);
-    __syncthreads();
-    BTD_STAMP(0);
-    // ---- l.7 / l.9 deferred left downdates (lower triangles) and their forward-sweep analogues
-    if (defC || defS) {
-        const int tri = n * (n + 1) / 2;
-        for (int q = tid; q < 2 * tri; q += blockDim.x) {
-            const bool second = q >= tri;
-            if (second ? !defS : !defC) continue;
-            if (!fact) continue;
-            const int qq = second ? q - tri : q;
-            // qq -> (i, jj), 0 <= jj <= i < n, by walking rows (n <= 32: at most 32 steps)
-            int i = 0, rem = qq;
-            while (rem > i) {
-                rem -= i + 1;
-                ++i;
-            }
-            const int jj = rem;
-            const T *M = second ? Ce : Cd;
-            T acc = T(0);
-            for (int k = 0; k < n; ++k) acc = fma(M[k * lda + i], M[k * lda + jj], acc);
-            T *dst = second ? Sep : A;
-            dst[i * lda + jj] -= acc;
-        }
-        if (solve) {
-            for (int q = tid; q < 2 * n * m; q += blockDim.x) {
-                const bool second = q >= n * m;
-                if (second ? !defS : !defC) continue;
-                const int qq = second ? q - n * m : q, i = qq / m, r = qq % m;
-                const T *M = second ? Ce : Cd;
-                const T *src = second ? yu : ys;
-                T acc = T(0);
-                for (int k = 0; k < n; ++k) acc = fma(M[k * lda + i], src[k * m + r], acc);
-                (second ? yt : yc)[qq] -= acc;
-            }
-        }
-        __syncthreads();
-    }
-    BTD_STAMP(1);
-    // ---- l.8 POTRF (one warp); other warps idle on the barrier
-    if (fact) {
-        if (warp == 0) {
-            // unrolled shuffle POTRF (btd_team.cuh), lane r = row r; rows/cols >= n: identity pad
-            const int r = tid & 31;
-            Lane<NB, 32> ln{r, 0};
-            T a[1][NB], di[1];
-#pragma unroll
-            for (int jj = 0; jj < NB; ++jj) a[0][jj] = (r < n && jj < n) ? A[r * lda + jj] : (r == jj ? T(1) : T(0));
-            const int bad = team_potrf<T, NB, 32, 1>(a, di, ln);
-            if (r < n) {
-#pragma unroll
-                for (int jj = 0; jj < NB; ++jj) A[r * lda + jj] = a[0][jj];
-                dinv[r] = di[0];
-            } else if (r < NB) {
-                dinv[r] = T(1);
-            }
-            if (r == 0) s_bad = (bad >= 0 && bad < n) ? bad : -1;
-        }
-        __syncthreads();
-        BTD_STAMP(2);
-        if (s_bad >= 0 && tid == 0) report_fail(info + sys, c);
-        T *dst = Dh + (size_t)(c - 1) * nn;
-        for (int q = tid; q < n * n; q += blockDim.x) dst[q] = A[(q / n) * lda + (q % n)];
-    } else {
-        for (int i = tid; i < n; i += blockDim.x) dinv[i] = rcp_fast(A[i * lda + i]);
-        __syncthreads();
-    }
-    // ---- l.10 / l.12 TRSMs: thread v < n solves row v of Cr, thread n + v column v of Cl;
-    //      threads 64 + r solve right-hand side r (Alg. 6 l.4)
-    if (fact && tid < 2 * n) {
-        const bool right = tid < n;
-        const int v = right ? tid : tid - n;
-        if (right ? hasR : hasL) {
-            T xv[NB];
-#pragma unroll
-            for (int k = 0; k < NB; ++k) xv[k] = k < n ? (right ? Cr[v * lda + k] : Cl[k * lda + v]) : T(0);
-            if (right)
-                thread_trsv_unrolled<T, NB>(xv, A, dinv, n, Cr + v * lda, 1);
-            else
-                thread_trsv_unrolled<T, NB>(xv, A, dinv, n, Cl + v, lda);
-        }
-    }
-    if (solve && tid >= 64) {
-        for (int r = tid - 64; r < m; r += blockDim.x - 64) {
-            T yv[NB];
-#pragma unroll
-            for (int k = 0; k < NB; ++k) yv[k] = k < n ? yc[k * m + r] : T(0);
-            thread_trsv_unrolled<T, NB>(yv, A, dinv, n, yc + r, m);
-        }
-    }
-    __syncthreads();
-    BTD_STAMP(3);
-    if (fact) {
-        if (hasR) {
-            T *dst = Cs + sR * nn;
-            for (int q = tid; q < n * n; q += blockDim.x) dst[q] = Cr[(q / n) * lda + (q % n)];
-        }
-        if (hasL) {
-            T *dst = Cs + sL * nn;
-            for (int q = tid; q < n * n; q += blockDim.x) dst[q] = Cl[(q / n) * lda + (q % n)];
-        }
-    }
-    if (solve)
-        for (int q = tid; q < n * m; q += blockDim.x) xs[(size_t)(c - 1) * n * m + q] = yc[q];
-    // ---- l.11 right downdate and l.13 fill (and the y push into y_{c+s})
-    if (fact && hasR) {
-        T *F = (hasL && hasR) ? Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn : nullptr;
-        for (int q = tid; q < 2 * n * n; q += blockDim.x) {
-            const bool fill = q >= n * n;
-            const int qq = fill ? q - n * n : q, i = qq / n, jj = qq % n;
-            if (fill) {
-                if (!F) continue;
-                T acc = T(0);
-                for (int k = 0; k < n; ++k) acc = fma(Cr[i * lda + k], Cl[k * lda + jj], acc);
-                F[qq] = -acc;
-            } else {
-                T acc = T(0);
-                for (int k = 0; k < n; ++k) acc = fma(Cr[i * lda + k], Cr[jj * lda + k], acc);
-                Dh[(size_t)(c + s - 1) * nn + qq] = Sep[i * lda + jj] - acc;
-            }
-        }
-    } else if (!fact && defS) {
-        // solve-only: nothing to downdate, y pushes below
-    }
-    if (solve && hasR) {
-        for (int q = tid; q < n * m; q += blockDim.x) {
-            const int i = q / m, r = q % m;
-            T acc = T(0);
-            for (int k = 0; k < n; ++k) acc = fma(Cr[i * lda + k], yc[k * m + r], acc);
-            xs[(size_t)(c + s - 1) * n * m + q] = yt[q] - acc;
-        }
-    }
-    __syncthreads();
-    BTD_STAMP(4);
-}
-
-
 // One column op of level l (Alg. 4 l.7-l.13 + Alg. 6 forward) by one CTA, built from the blocked
 // PERSIST2 pieces at panel width NB: blocks staged with 16-byte copies (ld NB+4, identity/zero
 // padded to NB), the deferred downdates (l.7, l.9), l.11 and the fill (l.13) as 8 x 8 tiles (DMMA
 // for fp64), the POTRF by one warp with the y rows riding along (Alg. 6 l.4), both TRSMs as one
 // batch of 2 NB vectors (rows of C_r, columns of C_l).
-template <typename T, int NB>
+// ATOMIC: Algorithm 5, the fully right-looking schedule -- no deferred
+// downdates; after its TRSMs the column pushes BOTH Schur updates, D~_{c-s} -= C_l^T C_l and
+// D~_{c+s} -= C_r C_r^T (lower triangles), and both forward-sweep updates into the separators'
+// y with atomic adds (contention <= 2). The per-level chain is potrf -> trsm -> syrk
+// (3 ops instead of 4); the summation order at a separator is nondeterministic (A7).
+template <typename T, int NB, bool ATOMIC = false>
 __device__ void wide_fwd_task2(const T *__restrict__ E, T *Dhat, T *C, T *x, int32_t *info, const Geo &g, int l,
                                long long sys, int j, bool fact, bool solve, T *sm
 #ifdef BTD_TIMING
@@ -364,8 +97,8 @@ __device__ void wide_fwd_task2(const T *__restrict__ E, T *Dhat, T *C, T *x, int
     const int s = 1 << (l - 1);
     const int c = s * (2 * j + 1);
     const bool hasL = c > s, hasR = c + s <= N;
-    const bool defC = l > 1 && (c + s / 2 <= N);
-    const bool defS = l > 1 && (c + s + s / 2 <= N);
+    const bool defC = !ATOMIC && l > 1 && (c + s / 2 <= N);
+    const bool defS = !ATOMIC && l > 1 && (c + s + s / 2 <= N);
     const T *Es = E ? E + sys * (size_t)(N - 1) * nn : nullptr;
     T *Dh = Dhat + sys * N * nn;
     T *Cs = C + sys * (size_t)g.nC * nn;
@@ -386,21 +119,23 @@ __device__ void wide_fwd_task2(const T *__restrict__ E, T *Dhat, T *C, T *x, int
     cta_issue_block<T>(A, LDW, Dh + (size_t)(c - 1) * nn, n, n, n);
     if (fact && hasR) {
         cta_issue_block<T>(Cr, LDW, CrSrc, n, n, n);
-        cta_issue_block<T>(Sep, LDW, Dh + (size_t)(c + s - 1) * nn, n, n, n);
+        if (!ATOMIC) cta_issue_block<T>(Sep, LDW, Dh + (size_t)(c + s - 1) * nn, n, n, n);
     }
     if (!fact && hasR) cta_issue_block<T>(Cr, LDW, Cs + sR * nn, n, n, n);
     if (defC) cta_issue_block<T>(Cd, LDW, Cs + cslot(g, l - 1, 2 * c / s) * nn, n, n, n);
     if (defS) cta_issue_block<T>(Ce, LDW, Cs + cslot(g, l - 1, 2 * c / s + 2) * nn, n, n, n);
     __pipeline_commit();
-    if (fact && hasL)  // columns of C_l, transposed (lanes over the contiguous index)
+    if ((fact || ATOMIC) && hasL) {  // columns of C_l, transposed (lanes over the contiguous index)
+        const T *src = fact ? ClSrc : Cs + sL * nn;
         for (int i = warp; i < n; i += nw)
-            for (int v = lane; v < n; v += 32) ClT[v * LDW + i] = ClSrc[(size_t)i * n + v];
+            for (int v = lane; v < n; v += 32) ClT[v * LDW + i] = src[(size_t)i * n + v];
+    }
     if (solve) {
         for (int q = tid; q < n * m; q += blockDim.x) {
             const int i = q / m, r = q % m;
             A[(NB + r) * LDW + i] = xs[(size_t)(c - 1) * n * m + q];
             if (defC) ys[q] = xs[(size_t)(c + s / 2 - 1) * n * m + q];
-            if (hasR) yt[q] = xs[(size_t)(c + s - 1) * n * m + q];
+            if (hasR && !ATOMIC) yt[q] = xs[(size_t)(c + s - 1) * n * m + q];
             if (defS) yu[q] = xs[(size_t)(c + s + s / 2 - 1) * n * m + q];
         }
         for (int q = tid; q < m * (NB - n); q += blockDim.x) A[(NB + q / (NB - n)) * LDW + n + q % (NB - n)] = T(0);
@@ -418,7 +153,7 @@ __device__ void wide_fwd_task2(const T *__restrict__ E, T *Dhat, T *C, T *x, int
     }
     if (fact && !hasR)
         for (int q = tid; q < NB * NB; q += blockDim.x) Cr[(q / NB) * LDW + q % NB] = T(0);
-    if (fact && !hasL)
+    if ((fact || ATOMIC) && !hasL)
         for (int q = tid; q < NB * NB; q += blockDim.x) ClT[(q / NB) * LDW + q % NB] = T(0);
     __pipeline_wait_prior(0);
     __syncthreads();
@@ -486,41 +221,95 @@ __device__ void wide_fwd_task2(const T *__restrict__ E, T *Dhat, T *C, T *x, int
     }
     if (solve)
         for (int q = tid; q < n * m; q += blockDim.x) xs[(size_t)(c - 1) * n * m + q] = A[(NB + q % m) * LDW + q / m];
-    // ---- l.11 right downdate  Sep -= Cr Cr^T  and l.13 fill  F = -Cr Cl  (8 x 8 tiles)
-    if (fact && hasR) {
+    if constexpr (ATOMIC) {
+        // ---- Alg. 5 l.9-l.11: S_R = C_r C_r^T (-> D~_{c+s}), S_L = C_l^T C_l (-> D~_{c-s}), fill
+        T *SR = Sep, *SL = Ce;
         const bool fill = hasL && hasR;
-        if (fill)
-            for (int q = tid; q < NB * NB; q += blockDim.x) F[(q / NB) * LDW + q % NB] = T(0);
-        __syncthreads();
-        for (int tt = warp; tt < ntri + (fill ? nt * nt : 0); tt += nw) {
-            if (tt < ntri) {
-                int ti = 0, q = tt;
-                while (q > ti) {
-                    q -= ti + 1;
-                    ++ti;
+        if (fact) {
+            for (int q = tid; q < NB * NB; q += blockDim.x) {
+                const int o = (q / NB) * LDW + q % NB;
+                SR[o] = T(0);
+                SL[o] = T(0);
+                F[o] = T(0);
+            }
+            __syncthreads();
+            for (int tt = warp; tt < 2 * ntri + (fill ? nt * nt : 0); tt += nw) {
+                if (tt < 2 * ntri) {
+                    const bool left = tt >= ntri;
+                    if (left ? !hasL : !hasR) continue;
+                    int ti = 0, q = left ? tt - ntri : tt;
+                    while (q > ti) {
+                        q -= ti + 1;
+                        ++ti;
+                    }
+                    const T *M = left ? ClT : Cr;  // C_l^T C_l = sum_k ClT[i][k] ClT[j][k]
+                    tile8_sub<T>(left ? SL : SR, LDW, 8 * ti, 8 * q, n, n, M, LDW, M, LDW, 0, n);
+                } else {
+                    const int t2 = tt - 2 * ntri;
+                    tile8_sub<T>(F, LDW, 8 * (t2 / nt), 8 * (t2 % nt), n, n, Cr, LDW, ClT, LDW, 0, n);
                 }
-                tile8_sub<T>(Sep, LDW, 8 * ti, 8 * q, n, n, Cr, LDW, Cr, LDW, 0, n);
-            } else {
-                const int t2 = tt - ntri;
-                tile8_sub<T>(F, LDW, 8 * (t2 / nt), 8 * (t2 % nt), n, n, Cr, LDW, ClT, LDW, 0, n);
+            }
+            __syncthreads();
+            // atomic pushes of the lower triangles (tiles hold -S); contention <= 2 per element
+            for (int i = warp; i < n; i += nw)
+                for (int jj = lane; jj <= i; jj += 32) {
+                    if (hasR) atomicAdd(Dh + (size_t)(c + s - 1) * nn + (size_t)i * n + jj, SR[i * LDW + jj]);
+                    if (hasL) atomicAdd(Dh + (size_t)(c - s - 1) * nn + (size_t)i * n + jj, SL[i * LDW + jj]);
+                }
+            if (fill) {
+                T *dF = Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn;
+                for (int i = warp; i < n; i += nw)
+                    for (int jj = lane; jj < n; jj += 32) dF[(size_t)i * n + jj] = F[i * LDW + jj];
             }
         }
-        __syncthreads();
-        T *dsep = Dh + (size_t)(c + s - 1) * nn;
-        for (int i = warp; i < n; i += nw)
-            for (int jj = lane; jj < n; jj += 32) dsep[(size_t)i * n + jj] = Sep[i * LDW + jj];
-        if (fill) {
-            T *dF = Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn;
-            for (int i = warp; i < n; i += nw)
-                for (int jj = lane; jj < n; jj += 32) dF[(size_t)i * n + jj] = F[i * LDW + jj];
+        if (solve) {  // y_{c+s} -= C_r y_c ; y_{c-s} -= C_l^T y_c   (atomic)
+            for (int q = tid; q < 2 * n * m; q += blockDim.x) {
+                const bool left = q >= n * m;
+                if (left ? !hasL : !hasR) continue;
+                const int qq = left ? q - n * m : q, i = qq / m, r = qq % m;
+                const T *M = left ? ClT : Cr;
+                T acc = T(0);
+                for (int k = 0; k < n; ++k) acc = fma(M[i * LDW + k], A[(NB + r) * LDW + k], acc);
+                atomicAdd(xs + (size_t)((left ? c - s : c + s) - 1) * n * m + qq, -acc);
+            }
         }
-    }
-    if (solve && hasR) {  // y_{c+s} = yt - C_r y_c
-        for (int q = tid; q < n * m; q += blockDim.x) {
-            const int i = q / m, r = q % m;
-            T acc = T(0);
-            for (int k = 0; k < n; ++k) acc = fma(Cr[i * LDW + k], A[(NB + r) * LDW + k], acc);
-            xs[(size_t)(c + s - 1) * n * m + q] = yt[q] - acc;
+    } else {
+        // ---- l.11 right downdate  Sep -= Cr Cr^T  and l.13 fill  F = -Cr Cl  (8 x 8 tiles)
+        if (fact && hasR) {
+            const bool fill = hasL && hasR;
+            if (fill)
+                for (int q = tid; q < NB * NB; q += blockDim.x) F[(q / NB) * LDW + q % NB] = T(0);
+            __syncthreads();
+            for (int tt = warp; tt < ntri + (fill ? nt * nt : 0); tt += nw) {
+                if (tt < ntri) {
+                    int ti = 0, q = tt;
+                    while (q > ti) {
+                        q -= ti + 1;
+                        ++ti;
+                    }
+                    tile8_sub<T>(Sep, LDW, 8 * ti, 8 * q, n, n, Cr, LDW, Cr, LDW, 0, n);
+                } else {
+                    const int t2 = tt - ntri;
+                    tile8_sub<T>(F, LDW, 8 * (t2 / nt), 8 * (t2 % nt), n, n, Cr, LDW, ClT, LDW, 0, n);
+                }
+            }
+            __syncthreads();
+            T *dsep = Dh + (size_t)(c + s - 1) * nn;
+            for (int i = warp; i < n; i += nw)
+                for (int jj = lane; jj < n; jj += 32) dsep[(size_t)i * n + jj] = Sep[i * LDW + jj];
+            if (fill) {
+                T *dF = Cs + cslot(g, l + 1, (c - s) / (2 * s)) * nn;
+                for (int i = warp; i < n; i += nw)
+                    for (int jj = lane; jj < n; jj += 32) dF[(size_t)i * n + jj] = F[i * LDW + jj];
+            }
+        }
+        if (solve && hasR) {  // y_{c+s} = yt - C_r y_c
+            for (int q = tid; q < n * m; q += blockDim.x) {
+                const int i = q / m, r = q % m;
+                T acc = T(0);
+                for (int k = 0; k < n; ++k) acc = fma(Cr[i * LDW + k], A[(NB + r) * LDW + k], acc);
+                xs[(size_t)(c + s - 1) * n * m + q] = yt[q] - acc;
+            }
         }
     }
     __syncthreads();
@@ -574,7 +363,7 @@ __device__ void wide_bwd_task(const T *Dhat, const T *C, T *x, const Geo &g, int
     __syncthreads();
 }
 
-template <typename T, int NB>
+template <typename T, int NB, bool ATOMIC = false>
 __global__ void __launch_bounds__(kWThreads, 1)
     btd_wide_kernel(const T *__restrict__ D, const T *__restrict__ E, const T *__restrict__ bvec, T *Dhat, T *C, T *x,
                     int32_t *info, Geo g, int batch, int fact, int solve) {
@@ -598,7 +387,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
     for (int l = 1; l <= g.L; ++l) {
         const int ncols = ((g.N >> (l - 1)) + 1) / 2;
         for (long long task = blockIdx.x; task < (long long)batch * ncols; task += gridDim.x)
-            wide_fwd_task2<T, NB>(E, Dhat, C, x, info, g, l, task / ncols, (int)(task % ncols), fact, solve, sm
+            wide_fwd_task2<T, NB, ATOMIC>(E, Dhat, C, x, info, g, l, task / ncols, (int)(task % ncols), fact, solve, sm
 #ifdef BTD_TIMING
                                  , btd_t_last
 #endif
