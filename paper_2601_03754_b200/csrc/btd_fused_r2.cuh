@@ -59,16 +59,28 @@ struct FusedR2Cfg {
     }
 };
 
-// Lane's rows of a padded-lower block: full-width vector loads (the tail of a short row reads the
-// next row's head, masked to zero -- never out of the block, since the last row is full width).
+// Lane's rows of a padded-lower block (entries above the diagonal read as zero).
 template <typename T, int NB, int TS, int RPL>
 __device__ __forceinline__ void pl_load_rows(T (&v)[RPL][NB], const T *blk, const Lane<NB, TS> &ln) {
+    constexpr int W = VecT<T>::W;
 #pragma unroll
     for (int t = 0; t < RPL; ++t) {
         const int i = ln.row(t);
-        vload<T, NB>(v[t], blk + PLow<T, NB>::off(i));
+        const T *p = blk + PLow<T, NB>::off(i);
+        // only the row's own chunks (w <= i): the next row belongs to another lane (no shared reads
+        // of words another lane may be storing)
 #pragma unroll
-        for (int j = 0; j < NB; ++j) v[t][j] = (j > i) ? T(0) : v[t][j];
+        for (int w = 0; w < NB; w += W) {
+            T tt[W];
+            if (w <= i) {
+                unpack(*reinterpret_cast<const typename VecT<T>::type *>(p + w), tt);
+            } else {
+#pragma unroll
+                for (int q = 0; q < W; ++q) tt[q] = T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < W; ++q) v[t][w + q] = (w + q > i) ? T(0) : tt[q];
+        }
     }
 }
 
@@ -370,12 +382,18 @@ __global__ void __launch_bounds__(NT *TS, MINB)
                     h_load_rows<T, NB, TS, RPL>(cr, Es + (size_t)(c - 1) * nn, ln, hasR, false, pf);
                     h_load_cols<T, NB, TS, RPL>(cl, Es + (size_t)((c >= 2 ? c : 2) - 2) * nn, ln, hasL, pf);
                 } else {
-                    pl_load_rows<T, NB, TS, RPL>(a, ES(c), ln);
+                    // inactive teams shadow column s, whose team may be writing D^_s into ES(s)
+                    if (act) pl_load_rows<T, NB, TS, RPL>(a, ES(c), ln);
                     s_load_rows<T, NB, TS, RPL>(cr, OS(hasR ? c + 1 : c - s + 1), ln);
                     s_load_cols<T, NB, TS, RPL>(cl, OS(c - s + 1), ln);
                 }
-                vload<T, NB>(yv, Y + (size_t)(c - 1) * LD);
-                if (!act) set_identity<T, NB, TS, RPL>(a, ln);
+                if (act) {  // inactive teams shadow column s: they must not read the y it is writing
+                    vload<T, NB>(yv, Y + (size_t)(c - 1) * LD);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NB; ++k) yv[k] = T(0);
+                    set_identity<T, NB, TS, RPL>(a, ln);
+                }
                 // -- a3 + a4 + a6 (Alg. 4 l.8, l.10, l.12; Alg. 6 l.4) in one sweep
                 const int bad = team_potrf_trsm<T, NB, TS, RPL, true>(a, cr, cl, yv, ln);
                 if (act && bad >= 0 && ln.q == 0) atomicMin(&s_fail, fail_key(c));
@@ -495,9 +513,10 @@ __global__ void __launch_bounds__(NT *TS, MINB)
                 T mine[RPL];
 #pragma unroll
                 for (int t = 0; t < RPL; ++t) {
-                    const T a = dot<T, NB>(crc[t], xr);   // (C_r^T x_{c+s})[i]
-                    const T b2 = dot<T, NB>(clr[t], xl);  // (C_l x_{c-s})[i]
-                    mine[t] = yc[ln.row(t)];
+                    // inactive teams (shadowing column s) read no y: column s's team is writing it
+                    const T a = hasR ? dot<T, NB>(crc[t], xr) : T(0);   // (C_r^T x_{c+s})[i]
+                    const T b2 = hasL ? dot<T, NB>(clr[t], xl) : T(0);  // (C_l x_{c-s})[i]
+                    mine[t] = act ? yc[ln.row(t)] : T(0);
                     mine[t] -= hasR ? a : T(0);
                     mine[t] -= hasL ? b2 : T(0);
                 }
@@ -512,11 +531,16 @@ __global__ void __launch_bounds__(NT *TS, MINB)
                 const T *pd = ES(c);
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
-                    T row[NB];
-                    vload<T, NB>(row, pd + PLow<T, NB>::off(i));  // row i: [0, i] valid
+                    const T *pr = pd + PLow<T, NB>::off(i);  // row i: its own chunks only
 #pragma unroll
-                    for (int k = 0; k <= i; ++k) Lf[i][k] = row[k];
-                    Linv[i] = rcp_fast(row[i]);
+                    for (int w = 0; w <= i; w += W) {
+                        T tt[W];
+                        unpack(*reinterpret_cast<const typename VecT<T>::type *>(pr + w), tt);
+#pragma unroll
+                        for (int q = 0; q < W; ++q)
+                            if (w + q <= i) Lf[i][w + q] = tt[q];
+                    }
+                    Linv[i] = rcp_fast(Lf[i][i]);
                 }
             } else {
                 const uint64_t pf = l2_evict_first();
@@ -537,7 +561,12 @@ __global__ void __launch_bounds__(NT *TS, MINB)
                 }
             }
             T v[NB];
-            vload<T, NB>(v, yc);
+            if (act) {
+                vload<T, NB>(v, yc);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NB; ++k) v[k] = T(0);
+            }
             bwd_full<T, NB>(v, Lf, Linv);
             __syncwarp();
             // x_c is final: write it to Y (read by the lower levels) and straight to HBM

@@ -417,7 +417,14 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                         s_load_rows<T, NB, TS, RPL>(cr, slots + (size_t)((hasR ? c + s / 2 : c) - 1) * BLK, ln);
                         s_load_cols<T, NB, TS, RPL>(cl, slots + (size_t)((hasL ? c - s / 2 : c) - 1) * BLK, ln);
                     }
-                    if (FY) vload<T, NB>(yv, Y + (size_t)(c - 1) * LD);
+                    if (FY) {  // inactive teams shadow column s: no reads of the y it is writing
+                        if (act) {
+                            vload<T, NB>(yv, Y + (size_t)(c - 1) * LD);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < NB; ++k) yv[k] = T(0);
+                        }
+                    }
                     // -- a3: D~_c -> D^_c
                     T a[RPL][NB];
                     s_load_rows<T, NB, TS, RPL>(a, slots + (size_t)(c - 1) * BLK, ln);
@@ -455,7 +462,12 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                     for (int q = 0; q < m; ++q) {
                         T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                         if constexpr (!FY) {
-                            vload<T, NB>(yv, yc);
+                            if (act) {
+                                vload<T, NB>(yv, yc);
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < NB; ++k) yv[k] = T(0);
+                            }
                             fwd_full<T, NB>(yv, Lf, Linv);
                         }
                         __syncwarp();
@@ -594,9 +606,10 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                     T mine[RPL];
 #pragma unroll
                     for (int t = 0; t < RPL; ++t) {
-                        const T a = dot<T, NB>(crc[t], xr);  // (C_r^T x_{c+s})[i]
-                        const T b2 = dot<T, NB>(clr[t], xl);  // (C_l x_{c-s})[i]
-                        mine[t] = yc[ln.row(t)];
+                        // inactive teams (shadowing column s) read no y: column s's team is writing it
+                        const T a = hasR ? dot<T, NB>(crc[t], xr) : T(0);   // (C_r^T x_{c+s})[i]
+                        const T b2 = hasL ? dot<T, NB>(clr[t], xl) : T(0);  // (C_l x_{c-s})[i]
+                        mine[t] = act ? yc[ln.row(t)] : T(0);
                         mine[t] -= hasR ? a : T(0);
                         mine[t] -= hasL ? b2 : T(0);
                     }
@@ -605,7 +618,12 @@ __global__ void __launch_bounds__(NT *TS, BTD_FR_MINB)
                     for (int t = 0; t < RPL; ++t)
                         if (act) yc[ln.row(t)] = mine[t];
                     __syncwarp();
-                    vload<T, NB>(v, yc);
+                    if (act) {
+                        vload<T, NB>(v, yc);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < NB; ++k) v[k] = T(0);
+                    }
                     bwd_full<T, NB>(v, Lf, Linv);
                     __syncwarp();
                     // x_c is final: write it to Y (read by the lower levels) and straight to HBM
@@ -771,8 +789,7 @@ __global__ void __launch_bounds__(NT *TS, FusedCfg<T, NB>::MINB)
                     for (int q = 0; q < m; ++q) {
                         T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                         T yv[RPL];
-                        yv[0] = yc[rv ? ln.q : 0];
-                        yv[0] = (act && rv) ? yv[0] : T(0);
+                        yv[0] = (act && rv) ? yc[ln.q] : T(0);  // inactive teams read no y
                         team_fwd<T, NB, TS, RPL>(yv, dl, dinv, ln);
                         if (act && rv) yc[ln.q] = yv[0];
                     }
@@ -830,10 +847,9 @@ __global__ void __launch_bounds__(NT *TS, FusedCfg<T, NB>::MINB)
                 for (int q = 0; q < m; ++q) {
                     T *yc = Y + ((size_t)(c - 1) * m + q) * LD;
                     T v[RPL];
-                    v[0] = yc[rv ? ln.q : 0];
-                    v[0] = (act && rv) ? v[0] : T(0);
-                    const T a = dot<T, NB>(crc[0], Y + ((size_t)((hasR ? c + s : c) - 1) * m + q) * LD);
-                    const T b2 = dot<T, NB>(clr[0], Y + ((size_t)((hasL ? c - s : c) - 1) * m + q) * LD);
+                    v[0] = (act && rv) ? yc[ln.q] : T(0);  // inactive teams read no y
+                    const T a = hasR ? dot<T, NB>(crc[0], Y + ((size_t)(c + s - 1) * m + q) * LD) : T(0);
+                    const T b2 = hasL ? dot<T, NB>(clr[0], Y + ((size_t)(c - s - 1) * m + q) * LD) : T(0);
                     v[0] -= hasR ? a : T(0);
                     v[0] -= hasL ? b2 : T(0);
                     team_bwd<T, NB, TS, RPL>(v, lc, dinv, ln);
