@@ -225,3 +225,106 @@ GENERATORS = {"dd": dd, "kalman": kalman}
 def make(kind: str, batch: int, N: int, n: int, m: int = 1, seed: int = 0, first_system: int = 0,
          device="cpu") -> Problem:
     return GENERATORS[kind](batch, N, n, m=m, seed=seed, first_system=first_system, device=device)
+
+
+# ----------------------------------------------------------------------------- extensions (§8(f) f4)
+
+@dataclass
+class ArrowProblem:
+    """Block-tridiagonal-arrow systems K = [[Psi, G^T], [G, Z]] (oracle/arrow.py), float64.
+
+    D, E, b as in ``Problem``; G: [B, N, n_a, n] (G[i-1] = border block of original block i);
+    Z: [B, n_a, n_a]; ba: [B, n_a, m]; xstar / xastar: the solution used to build (b, ba).
+    """
+
+    D: torch.Tensor
+    E: torch.Tensor
+    G: torch.Tensor
+    Z: torch.Tensor
+    b: torch.Tensor
+    ba: torch.Tensor
+    xstar: torch.Tensor
+    xastar: torch.Tensor
+
+    def cast(self, dtype):
+        return ArrowProblem(*(t.to(dtype).contiguous() for t in (self.D, self.E, self.G, self.Z, self.b, self.ba)),
+                            self.xstar, self.xastar)
+
+    def to(self, device):
+        return ArrowProblem(*(t.to(device) for t in (self.D, self.E, self.G, self.Z, self.b, self.ba,
+                                                      self.xstar, self.xastar)))
+
+
+def arrow(batch: int, N: int, n: int, na: int, m: int = 1, seed: int = 0, first_system: int = 0,
+          device="cpu") -> ArrowProblem:
+    """``dd`` block-tridiagonal part plus a border: G_i entries uniform[-1,1] / sqrt(N n) (so
+    ||G||_F^2 <= n_a), Z = S_Z + (4 n_a + 1) I with S_Z symmetric uniform[-1,1]. Provably SPD:
+    lambda_min(Psi) >= 1 (A18) and lambda_min(Z) >= n_a + 1 > ||G Psi^{-1} G^T||."""
+    base = dd(batch, N, n, m=m, seed=seed, first_system=first_system, device=device)
+    sys_ = _systems(batch, first_system, device)
+    c0 = (2 * N + 2) * n * n + 2 * N * n * m + 1_000_003
+    cG = torch.arange(N * na * n, dtype=torch.int64, device=device) + c0
+    G = uniform(seed, sys_[:, None], cG[None, :]).reshape(batch, N, na, n) / math.sqrt(N * n)
+    cZ = torch.arange(na * na, dtype=torch.int64, device=device) + c0 + N * na * n
+    U = uniform(seed, sys_[:, None], cZ[None, :]).reshape(batch, na, na)
+    Z = torch.tril(U) + torch.tril(U, -1).transpose(-1, -2) + (4 * na + 1) * torch.eye(
+        na, dtype=torch.float64, device=device)
+    cx = torch.arange(na * m, dtype=torch.int64, device=device) + c0 + N * na * n + na * na
+    xa = normal(seed, sys_[:, None], cx[None, :]).reshape(batch, na, m)
+    xs = base.xstar
+    # b = Psi x* + G^T x_a*,  b_a = G x* + Z x_a*
+    b = block_tridiag_matvec(base.D, base.E, xs) + G.transpose(-1, -2) @ xa[:, None]
+    ba = torch.einsum("bian,binm->bam", G, xs) + Z @ xa
+    return ArrowProblem(base.D, base.E, G, Z, b, ba, xs, xa)
+
+
+@dataclass
+class BandedProblem:
+    """Block-banded systems of block bandwidth w (oracle/banded.py), float64.
+
+    D: [B, N, n, n]; A: [B, w, N, n, n] with A[:, k-1, i-1] = block (i+k, i) (entries with
+    i + k > N are zero and never read); b, xstar: [B, N, n, m].
+    """
+
+    D: torch.Tensor
+    A: torch.Tensor
+    b: torch.Tensor
+    xstar: torch.Tensor
+
+    def cast(self, dtype):
+        return BandedProblem(self.D.to(dtype).contiguous(), self.A.to(dtype).contiguous(),
+                             self.b.to(dtype).contiguous(), self.xstar)
+
+    def to(self, device):
+        return BandedProblem(self.D.to(device), self.A.to(device), self.b.to(device), self.xstar.to(device))
+
+
+def banded_matvec(D: torch.Tensor, A: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    """Psi_w x (float64): y_i = D_i x_i + sum_k (A_k[i-k] x_{i-k} + A_k[i]^T x_{i+k})."""
+    y = D @ x
+    N = D.shape[1]
+    for k in range(1, A.shape[1] + 1):
+        if N > k:
+            Ak = A[:, k - 1, :N - k]
+            y[:, k:] += Ak @ x[:, :N - k]
+            y[:, :N - k] += Ak.transpose(-1, -2) @ x[:, k:]
+    return y
+
+
+def banded(batch: int, N: int, n: int, w: int, m: int = 1, seed: int = 0, first_system: int = 0,
+           device="cpu") -> BandedProblem:
+    """D_i = S_i + ((2w+1) n + 1) I (S_i symmetric uniform[-1,1]), A_k[i] uniform[-1,1]:
+    Gershgorin gives lambda_min >= 1 (the w = 1 case is ``dd``'s shift 3n+1)."""
+    sys_ = _systems(batch, first_system, device)
+    nn = n * n
+    cD = torch.arange(N * nn, dtype=torch.int64, device=device)
+    U = uniform(seed, sys_[:, None], cD[None, :]).reshape(batch, N, n, n)
+    D = torch.tril(U) + torch.tril(U, -1).transpose(-1, -2) + ((2 * w + 1) * n + 1) * torch.eye(
+        n, dtype=torch.float64, device=device)
+    cA = torch.arange(w * N * nn, dtype=torch.int64, device=device) + N * nn
+    A = uniform(seed, sys_[:, None], cA[None, :]).reshape(batch, w, N, n, n)
+    for k in range(1, w + 1):
+        A[:, k - 1, max(N - k, 0):] = 0.0
+    cx = torch.arange(N * n * m, dtype=torch.int64, device=device) + (w + 1) * N * nn
+    xs = normal(seed, sys_[:, None], cx[None, :]).reshape(batch, N, n, m)
+    return BandedProblem(D, A, banded_matvec(D, A, xs), xs)

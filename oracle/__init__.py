@@ -15,6 +15,10 @@ Contents:
                 discovering fill symbolically (numpy); knows nothing about levels.
 * ``layout`` -- mapping of a factor L^ onto the C-ABI (Dhat, C) layout (include/btd.h).
 * ``metrics``-- the error measures of SURVEY.md §8(c) A16.
+* ``refine`` -- §8(f) f4: classical iterative refinement on a binary32 factorization.
+* ``arrow``  -- §8(f) f4: block-tridiagonal-arrow systems, dense definitions.
+* ``banded`` -- §8(f) f4: block-banded systems, dense definitions + reblocking.
+* ``partition`` -- §8(f) f3: partition permutation, Proposition 1 and Algorithm 2 line by line.
 
 Parity status per function is listed in DESIGN.md ("Oracle pins").
 """
