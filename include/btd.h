@@ -140,6 +140,83 @@ btd_status btd_factor_solve_host(const btd_plan *plan, const void *host_D, const
                                  void *dev_Dhat, void *dev_C, void *dev_x, int32_t *dev_info,
                                  int32_t chunks, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Extensions (csrc/btd_ext.cu). Each one reuses the core
+ * factor/solve above for its O(N n^3) work; its own kernels are the packing,
+ * residual and border steps named below.
+ * ------------------------------------------------------------------------- */
+
+/* f4a mixed precision ("mixed-precision strategies"; R8):
+ * classical iterative refinement on a binary32 factorization. `plan` must be a
+ * BTD_F32 plan of the system's (N, n, batch, m). Inputs D, E, b are binary64
+ * device arrays in the layouts above; Dhat, C receive the binary32 factor of
+ * fl32(Psi); x [batch][N][n][m] (binary64) receives x_iters, where
+ *   x_0 = solve32(fl32(b)),  x_k = x_{k-1} + solve32(fl32(b - Psi x_{k-1}))
+ * with the residual formed in binary64. resid (optional, binary64 [batch]):
+ * ||b - Psi x_iters||_2 / ||b||_2 per system (summation order not deterministic).
+ * work: device workspace of btd_mixed_workspace_bytes() bytes, 16-byte aligned,
+ * owned by the caller, not read across calls. Launches: 3 + 1 + 2*iters + 1
+ * (+1 with resid). info as btd_factor (the binary32 pivots). */
+btd_status btd_mixed_workspace_bytes(const btd_plan *plan, size_t *bytes);
+btd_status btd_mixed_factor_solve(const btd_plan *plan, const double *D, const double *E, const double *b,
+                                  float *Dhat, float *C, double *x, int32_t *info, int32_t iters, double *resid,
+                                  void *work, void *stream);
+
+/* f4b arrowhead ("arrow structures"; R9): solves
+ *   [[Psi, G^T], [G, Z]] [x; x_a] = [b; b_a]
+ * with the border eliminated last (ordering diag(P_inf, I)). `plan` is the plan
+ * of Psi with m = na + mb (the border columns ride as extra right-hand sides).
+ * G [batch][N][na][n] (G[i-1] = border block of original block i), Z [batch][na][na]
+ * (lower triangle read), b [batch][N][n][mb], b_a [batch][na][mb].
+ * Outputs: Dhat, C (factor of Psi, layout above); Y [batch][N][n][na+mb] =
+ * Psi^{-1} [G^T | b] (its first na columns are V = Psi^{-1} G^T); LZ [batch][na][na]
+ * = chol(Z - G V) (strict upper zero); x [batch][N][n][mb]; x_a [batch][na][mb].
+ * R [batch][N][n][na+mb] is caller workspace. info[j] = N + 1 if the border
+ * Schur complement is not positive definite (and Psi was). Needs na*(na+mb)
+ * elements of shared memory (<= 227 KB). Launches: 4. */
+btd_status btd_arrow_factor_solve(const btd_plan *plan, int64_t na, const void *D, const void *E, const void *G,
+                                  const void *Z, const void *b, const void *ba, void *Dhat, void *C, void *R, void *Y,
+                                  void *LZ, void *x, void *xa, int32_t *info, void *stream);
+
+/* f4c block banded, bandwidth w ("block banded matrices with larger
+ * bandwidth"; R11): D [batch][N][n][n], A [batch][w][N][n][n] with
+ * A[k-1][i-1] = block (i+k, i) of Psi_w, b, x [batch][N][n][m]. The system is
+ * solved as the block-tridiagonal matrix of super-blocks of w consecutive blocks
+ * (N' = ceil(N/w) super-blocks of size w n, identity padding). `plan` is the plan
+ * of (N', w n, batch, m). Caller workspace: Dp [batch][N'][wn][wn], Ep
+ * [batch][N'-1][wn][wn], bp, xp [batch][N'][wn][m]. Outputs: Dhat, C (factor of
+ * the super-block system, layout above), x, info (super-block pivot index).
+ * Launches: 3. */
+btd_status btd_banded_factor_solve(const btd_plan *plan, int64_t N, int64_t n, int64_t w, const void *D,
+                                   const void *A, const void *b, void *Dp, void *Ep, void *bp, void *Dhat, void *C,
+                                   void *xp, void *x, int32_t *info, void *stream);
+
+/* f3 partition permutation (Algorithm 2; R10), one
+ * chunk per call so that each rank of a multi-GPU job runs its own chunk:
+ * chunk k holds N_k consecutive blocks (D [N_k][n][n], E [N_k-1][n][n], b
+ * [N_k][n][m]); its left pivot A_k sits before it, its right pivot A_{k+1}
+ * after it. Bk = Psi[D_1k, A_k] and Ak, ak (pivot diagonal block and rhs
+ * [n][m]) are NULL for the first chunk; Fk = Psi[A_{k+1}, D_{N_k k}] is NULL
+ * for the last. `plan` is the chunk's plan with batch 1 and m = nb + nf + m_b
+ * (nb = n if Bk, nf = n if Fk).
+ * btd_partition_local: R (workspace) = [B_k e_1 | F_k^T e_N | b], factor and
+ *   solve the chunk (Dhat, C, Y = Psi_k^{-1} R), and write the chunk's packet
+ *   (3 n^2 + 2 n m_b elements): A_k - B_k^T Psi_k^{-1} B_k | F_k Psi_k^{-1} F_k^T |
+ *   -F_k Psi_k^{-1} B_k | a_k - B_k^T Psi_k^{-1} b | F_k Psi_k^{-1} b.
+ * btd_partition_reduce: from the p packets (chunk order, contiguous) assemble the
+ *   block-tridiagonal pivot system (p-1 blocks: DS, ES, bS) and factor/solve it
+ *   (plan ps: N = p-1, batch 1, m = m_b) -> xS = pivot solutions.
+ * btd_partition_finish: x = Y[:, b] - Y[:, B] xL - Y[:, F] xR with xL = xS[k-2]
+ *   (NULL for the first chunk) and xR = xS[k-1] (NULL for the last).
+ * Launches: local 3, reduce 2, finish 1. */
+btd_status btd_partition_local(const btd_plan *plan, const void *D, const void *E, const void *Bk, const void *Fk,
+                               const void *Ak, const void *ak, const void *b, void *R, void *Dhat, void *C, void *Y,
+                               void *packet, int32_t *info, void *stream);
+btd_status btd_partition_reduce(const btd_plan *ps, int32_t p, const void *packets, void *DS, void *ES, void *bS,
+                                void *DhatS, void *CS, void *xS, int32_t *infoS, void *stream);
+btd_status btd_partition_finish(const btd_plan *plan, const void *Y, const void *xL, const void *xR, void *x,
+                                void *stream);
+
 const char *btd_status_string(btd_status status);
 /* Last CUDA error string observed by this thread inside the library (or ""). */
 const char *btd_last_error(void);

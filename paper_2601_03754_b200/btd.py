@@ -45,6 +45,13 @@ SIGNATURES = [
     ("btd_solve", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("btd_factor_solve", ctypes.c_int, [_vp] * 9),
     ("btd_factor_solve_host", ctypes.c_int, [_vp] * 15 + [_i32, _vp]),
+    ("btd_mixed_workspace_bytes", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_size_t)]),
+    ("btd_mixed_factor_solve", ctypes.c_int, [_vp] * 8 + [_i32, _vp, _vp, _vp]),
+    ("btd_arrow_factor_solve", ctypes.c_int, [_vp, _i64] + [_vp] * 15),
+    ("btd_banded_factor_solve", ctypes.c_int, [_vp, _i64, _i64, _i64] + [_vp] * 12),
+    ("btd_partition_local", ctypes.c_int, [_vp] * 15),
+    ("btd_partition_reduce", ctypes.c_int, [_vp, _i32] + [_vp] * 9),
+    ("btd_partition_finish", ctypes.c_int, [_vp] * 6),
     ("btd_status_string", ctypes.c_char_p, [ctypes.c_int]),
     ("btd_last_error", ctypes.c_char_p, []),
 ]

@@ -76,7 +76,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, t
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     units = [(os.path.join(CSRC, "btd.cu"), [], os.path.join(OBJ, "btd.o")),
-             (os.path.join(CSRC, "btd_persist.cu"), [], os.path.join(OBJ, "btd_persist.o"))]
+             (os.path.join(CSRC, "btd_persist.cu"), [], os.path.join(OBJ, "btd_persist.o")),
+             (os.path.join(CSRC, "btd_ext.cu"), [], os.path.join(OBJ, "btd_ext.o"))]
     for dt in DTYPES:
         for nb in SIZES:
             units.append((os.path.join(CSRC, "btd_inst.cu"), [f"-DBTD_T={dt}", f"-DBTD_NB={nb}"],

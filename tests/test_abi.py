@@ -208,3 +208,38 @@ def test_fused_r2_slot_schedule_is_race_free(N):
     assert all(v[0] == "cache" for v in live.values())
     if N == 128:
         assert LC == 3
+
+
+def test_extension_entry_points_validate_before_launch():
+    """§8(f) entry points (csrc/btd_ext.cu) reject bad arguments on the host, without a GPU."""
+    import ctypes
+
+    L = btd.lib()
+    p64 = btd.Plan(16, 4, 2, 1, torch.float64)
+    p32 = btd.Plan(16, 4, 2, 1, torch.float32)
+    sz = ctypes.c_size_t(0)
+    assert L.btd_mixed_workspace_bytes(p64.handle, ctypes.byref(sz)) == 1          # needs a binary32 plan
+    assert L.btd_mixed_workspace_bytes(p32.handle, ctypes.byref(sz)) == 0
+    nn, nx = 16, 2 * 16 * 4
+    expect = sum(((v + 255) // 256) * 256 for v in (2 * 16 * nn * 4, 2 * 15 * nn * 4, nx * 4, nx * 4, nx * 8, 2 * 2 * 8))
+    assert sz.value == expect
+    fake = ctypes.c_void_p(4096)  # never dereferenced: every call below fails its checks first
+    # mixed: iters < 0, misaligned x
+    assert L.btd_mixed_factor_solve(p32.handle, fake, fake, fake, fake, fake, fake, fake, -1, None, fake, None) == 1
+    assert L.btd_mixed_factor_solve(p32.handle, fake, fake, fake, fake, fake, ctypes.c_void_p(4100), fake, 1, None,
+                                    fake, None) == 1
+    # arrow: na must leave at least one rhs column (plan m = na + mb)
+    pa = btd.Plan(16, 4, 2, 3, torch.float64)
+    assert L.btd_arrow_factor_solve(pa.handle, 3, *([fake] * 14), None) == 1
+    assert L.btd_arrow_factor_solve(pa.handle, 0, *([fake] * 14), None) == 1
+    # banded: the plan must be the super-block plan (ceil(N/w), w n)
+    pb = btd.Plan(5, 12, 1, 1, torch.float64)
+    assert L.btd_banded_factor_solve(pb.handle, 13, 4, 2, *([fake] * 11), None) == 1
+    assert L.btd_banded_factor_solve(pb.handle, 16, 4, 3, *([fake] * 11), None) == 1
+    # partition: batch must be 1; reduce needs p >= 2 and a plan of p - 1 blocks
+    assert L.btd_partition_local(p64.handle, *([fake] * 13), None) == 1
+    ps = btd.Plan(3, 4, 1, 1, torch.float64)
+    assert L.btd_partition_reduce(ps.handle, 3, *([fake] * 8), None) == 1
+    assert L.btd_partition_reduce(ps.handle, 1, *([fake] * 8), None) == 1
+    pc = btd.Plan(8, 4, 1, 1, torch.float64)
+    assert L.btd_partition_finish(pc.handle, fake, fake, None, fake, None) == 1    # m = 1 - n < 1
