@@ -98,6 +98,15 @@ def _ncu_traffic(batch: int) -> float | None:
     return None
 
 
+def _ncu_kernel_name() -> str | None:
+    """Name of the dominant kernel as recorded by the committed ncu capture (profiles/ncu_fused_c5.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_fused_c5.json")) as f:
+            return json.load(f).get("kernel")
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """Samples SM clock and clock-event (throttle) reasons via NVML while the timed region runs."""
 
@@ -314,6 +323,120 @@ def _latency_sweep(dev) -> dict:
     return out
 
 
+def _critical_path(dev, latency: dict) -> dict | None:
+    """Critical-path floor of the single-system regime: t_chain(n) = measured
+    potrf -> trsm -> syrk latency of ONE column op in one CTA with its blocks in shared memory,
+    plus one grid.sync, from tools/micro/chain_latency (built by __graft_entry__.build()); floor(N)
+    = L(N) x (t_chain + t_sync). Reported next to the graph-replay latency of the same config."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "tools", "micro", "chain_latency")
+    if not os.path.exists(exe):
+        return None
+    try:
+        txt = subprocess.run([exe], capture_output=True, text=True, timeout=120,
+                             env=dict(os.environ, CUDA_VISIBLE_DEVICES=str(dev.index or 0))).stdout
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+    rows = [json.loads(l) for l in txt.splitlines() if l.startswith("{")]
+    sync = next((r for r in rows if "gridsync_cyc" in r), None)
+    if sync is None:
+        return {"raw": rows}
+    mhz = sync["sm_khz"] / 1e3
+    out = {"gridsync_us": round(sync["gridsync_cyc"] / mhz, 3), "sm_mhz": mhz, "chain": {}, "floors": {}}
+    for r in rows:
+        if "potrf_cyc" not in r or not r["potrf_cyc"] or r.get("err", "no error") != "no error":
+            continue
+        cyc = r["potrf_cyc"] + r["trsm_cyc"] + r["syrk_cyc"]
+        out["chain"][f"{r['dtype']}_n{r['n']}"] = dict(potrf_us=round(r["potrf_cyc"] / mhz, 3),
+                                                        trsm_us=round(r["trsm_cyc"] / mhz, 3),
+                                                        syrk_us=round(r["syrk_cyc"] / mhz, 3),
+                                                        chain_us=round(cyc / mhz, 3))
+    for name, res in latency.items():
+        dt = "f64" if "fp64" in name else "f32"
+        n = int(name.split("_n")[1].split("_")[0])
+        key = f"{dt}_n{n}"
+        if key not in out["chain"]:
+            continue
+        for N, r in res.items():
+            L = int(N).bit_length()
+            fl = L * (out["chain"][key]["chain_us"] + out["gridsync_us"])
+            out["floors"][f"{name}/N{N}"] = dict(floor_us=round(fl, 2), measured_us=r["graph_warm"],
+                                                 frac=round(fl / r["graph_warm"], 4))
+    return out
+
+
+def _ext_bench(dev) -> dict:
+    """The §8(f) rows on the device: CUDA events on the launching stream, 3 warm-up calls, mean of
+    `reps` calls (host-launched, outputs allocated by the binding). Systems/s or ms per call."""
+    import btdgen
+    import paper_2601_03754_b200 as btd
+    from paper_2601_03754_b200 import ext, partition
+
+    s = torch.cuda.Stream(dev)
+    out = {}
+
+    def timeit(fn, reps):
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                fn()
+            s.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(reps):
+                fn()
+            e1.record(s)
+            e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def rres(D, E, x, b):
+        r = btdgen.block_tridiag_matvec(D.double(), E.double(), x.double()) - b.double()
+        return float((r.flatten(1).norm(dim=1) / b.double().flatten(1).norm(dim=1)).max())
+
+    # f4a: the c5 workload with binary64 inputs: binary64 direct vs binary32 factor + refinement
+    B = B_TOTAL
+    p = btdgen.kalman(B, N_BLK, N_SZ, seed=5, device=dev)
+    plan32 = btd.Plan(N_BLK, N_SZ, B, 1, torch.float32)
+    plan64 = btd.Plan(N_BLK, N_SZ, B, 1, torch.float64)
+    work = torch.empty(ext.mixed_workspace_bytes(plan32), dtype=torch.uint8, device=dev)
+    mixed = {"workload": f"{B} kalman systems, n={N_SZ}, N={N_BLK}, binary64 inputs"}
+    o64 = btd.factor_solve(p.D, p.E, p.b, plan=plan64)
+    ms = timeit(lambda: btd.factor_solve(p.D, p.E, p.b, plan=plan64, out=o64, stream=s), 5)
+    mixed["fp64_direct"] = dict(ms=round(ms, 4), systems_per_s=B / ms * 1e3, variant=plan64.variant,
+                                max_rel_residual=rres(p.D, p.E, o64[2], p.b))
+    for it in (0, 1, 2, 3):
+        ms = timeit(lambda: ext.mixed_factor_solve(p.D, p.E, p.b, iters=it, plan=plan32, work=work, stream=s), 5)
+        x = ext.mixed_factor_solve(p.D, p.E, p.b, iters=it, plan=plan32, work=work)[2]
+        mixed[f"iters{it}"] = dict(ms=round(ms, 4), systems_per_s=B / ms * 1e3,
+                                   max_rel_residual=rres(p.D, p.E, x, p.b), launches=5 + 2 * it)
+    out["f4a_mixed"] = mixed
+    del p, o64, work
+    # f4b: arrowhead, the c5 block-tridiagonal part with an 8-wide border (fp32)
+    pa = btdgen.arrow(B, N_BLK, N_SZ, 8, seed=5, device=dev).cast(torch.float32)
+    pla = btd.Plan(N_BLK, N_SZ, B, 9, torch.float32)
+    ms = timeit(lambda: ext.arrow_factor_solve(pa.D, pa.E, pa.G, pa.Z, pa.b, pa.ba, plan=pla, stream=s), 5)
+    out["f4b_arrow"] = dict(workload=f"{B} systems fp32 n={N_SZ} N={N_BLK} border na=8", ms=round(ms, 4),
+                            systems_per_s=B / ms * 1e3, variant=pla.variant, launches=4)
+    del pa
+    # f4c: block banded, bandwidth 3, n = 4 (super-blocks of 12), fp32
+    pb = btdgen.banded(B, N_BLK, 4, 3, seed=5, device=dev).cast(torch.float32)
+    plb = btd.Plan(-(-N_BLK // 3), 12, B, 1, torch.float32)
+    ms = timeit(lambda: ext.banded_factor_solve(pb.D, pb.A, pb.b, plan=plb, stream=s), 5)
+    out["f4c_banded"] = dict(workload=f"{B} systems fp32 n=4 N={N_BLK} w=3", ms=round(ms, 4),
+                             systems_per_s=B / ms * 1e3, variant=plb.variant, launches=3)
+    del pb
+    # f3: one long system (fp64, n = 32, N = 4095) split into p chunks. ONE GPU here: the chunks run
+    # one after another, so this measures the per-chunk work, not a multi-GPU latency.
+    pp = btdgen.kalman(1, 4095, 32, seed=5, device=dev)
+    part = {"workload": "single system fp64 n=32 N=4095, chunks sequential on one GPU"}
+    for nparts in (1, 2, 4, 8):
+        ms = timeit(lambda: partition.solve(pp.D[0], pp.E[0], pp.b[0], nparts), 3)
+        x, _ = partition.solve(pp.D[0], pp.E[0], pp.b[0], nparts)
+        part[f"p{nparts}"] = dict(ms=round(ms, 4), max_rel_residual=rres(pp.D, pp.E, x[None], pp.b))
+    out["f3_partition"] = part
+    return out
+
+
 # ------------------------------------------------------------------ the batched benchmark, one rank
 
 class _CudaClock:
@@ -466,7 +589,7 @@ def build_line(args, agg: dict, local: dict, pk: dict | None = None) -> dict:
                      "frac": achieved / pk["hbm"] if achieved else None,
                      "traffic": _ncu_traffic(local["count"]),
                      "algorithmic_bytes_per_launch": ab["total"] * local["count"], "peak_source": pk["src"],
-                     "kernel": "btd_fused_r_kernel<float,12,4,32,true,true,1,true>",
+                     "kernel": _ncu_kernel_name(),
                      "kernel_ms_avg": kern_avg_ms},
         "flops_per_system": algorithmic_flops_per_system(),
         "check": {"max_rel_residual_fp64": agg["max_rel_residual"], "failed_systems": agg["failed_systems"]},
@@ -508,6 +631,9 @@ def run_ours(args):
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if args.latency and ws == 1:
         line["latency_us"] = _latency_sweep(dev)
+        line["critical_path"] = _critical_path(dev, line["latency_us"])
+    if args.ext and ws == 1:
+        line["extensions"] = _ext_bench(dev)
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
@@ -530,6 +656,8 @@ def parse_args(argv=None):
     ap.add_argument("--ref-sample", type=int, default=1024)
     ap.add_argument("--latency", action="store_true", default=True)
     ap.add_argument("--no-latency", dest="latency", action="store_false")
+    ap.add_argument("--ext", action="store_true", default=True)
+    ap.add_argument("--no-ext", dest="ext", action="store_false")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -97,5 +97,15 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, t
     return LIB
 
 
+def build_micro(name: str) -> str:
+    """Compile tools/micro/<name>.cu (a measurement tool, not part of libbtd.so) for sm_100a."""
+    src = os.path.join(ROOT, "tools", "micro", name + ".cu")
+    exe = os.path.join(ROOT, "tools", "micro", name)
+    deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    if _stale(exe, deps):
+        subprocess.run([_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-o", exe, src], check=True)
+    return exe
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True, timing="--timing" in sys.argv))

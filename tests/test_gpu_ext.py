@@ -52,7 +52,9 @@ def test_mixed_refinement_reaches_binary64(gen, B, N, n, m):
         assert metrics.err_x(xs[j], xo) <= 1e-10
         r = metrics.residual(Dj, Ej, xs[j], bj)
         assert r <= 1e-12
-        assert abs(float(resid[j]) - r) <= 1e-3 * r + 1e-17      # the library's own residual report
+        # the library's own residual report: at this level the residual is rounding noise of its
+        # own evaluation (different summation orders), so only its size is comparable
+        assert float(resid[j]) <= 1e-12 and float(resid[j]) <= 4 * r + 1e-15
     # the binary32 factor is the factor of fl32(Psi) (A17 tolerance vs the fp64 oracle)
     j = B - 1
     D32, E32 = prob.D[j].float().double().numpy(), prob.E[j].float().double().numpy()
@@ -66,13 +68,17 @@ def test_mixed_zero_iterations_is_the_binary32_path():
     dev = _dev()
     prob = btdgen.kalman(6, 50, 12, seed=9)
     D, E, b = prob.D.to(dev), prob.E.to(dev), prob.b.to(dev)
-    Dh, C, x, info, _ = ext.mixed_factor_solve(D, E, b, iters=0)
+    Dh, C, x, info, res0 = ext.mixed_factor_solve(D, E, b, iters=0, want_resid=True)
     Dh32, C32, x32, _ = btd.factor_solve(D.float(), E.float(), b.float())
     torch.cuda.synchronize()
     assert torch.equal(Dh, Dh32) and torch.equal(C, C32)
     assert torch.equal(x, x32.double())
     x0, _, _ = refine.refine(prob.D[2].numpy(), prob.E[2].numpy(), prob.b[2].numpy(), iters=0)
     assert metrics.err_x(x[2].cpu().numpy(), x0) <= 1e-4
+    # a binary32-level residual is far above the evaluation noise: the report matches closely
+    for j in range(6):
+        r = metrics.residual(prob.D[j].numpy(), prob.E[j].numpy(), x[j].cpu().numpy(), prob.b[j].numpy())
+        assert 1e-9 < r < 1e-5 and abs(float(res0[j]) - r) <= 1e-6 * r
 
 
 def test_mixed_error_contracts_per_iteration():
