@@ -38,15 +38,17 @@ __global__ void __launch_bounds__(256, 1) k_op(const T *Ag, unsigned long long *
     unsigned long long t0 = 0;
     for (int rep = 0; rep < 2; ++rep) {
         Bufs<T, NP, VT>::setup(reinterpret_cast<T *>(raw), Ag, A, X, S, dinv);
-        if (OP == 1 || OP == 3) {  // the TRSM / back substitution need a factor: factor untimed
-            cta_potrf_blocked<T, Q>(A, LD, n, NP, 0, dinv);
-            __syncthreads();
-        }
+        // OP 1 / 3 (TRSM, back substitution) get an already factored A from k_factor: a factorization
+        // in the same kernel raises register pressure and made the TRSM spill (3.5 KB stack), which
+        // the library kernels (btd_wide_kernel: no stack) do not.
         t0 = clock64();
         if (OP == 0) {
             cta_potrf_blocked<T, Q>(A, LD, n, NP, 1, dinv);  // + one y row
         } else if (OP == 1) {
-            cta_trsm_blocked<T, Q>(X, LD, VT, A, LD, NP, dinv);
+            // sizes as runtime values, as in the library's call sites (compile-time constants let
+            // the compiler hoist every L element into registers and spill)
+            const int rt = n < 0;
+            cta_trsm_blocked<T, Q>(X, LD + rt, VT + rt, A, LD + rt, NP + rt, dinv);
         } else if (OP == 2) {  // S -= X X^T (lower 8 x 8 tiles), the l.11 downdate
             const int m = VT < n ? VT : n, nt = (m + 7) / 8, ntri = nt * (nt + 1) / 2;
             for (int tt = threadIdx.x >> 5; tt < ntri; tt += blockDim.x >> 5) {
@@ -79,6 +81,18 @@ __global__ void __launch_bounds__(256, 1) k_op(const T *Ag, unsigned long long *
     if (threadIdx.x == 0) out[OP] = clock64() - t0;
 }
 
+// The factor L of A (in place, lower triangle; A's diagonal is replaced by L's) for OP 1 / 3.
+template <typename T, int NP, int VT>
+__global__ void __launch_bounds__(256, 1) k_factor(const T *Ag, T *Lg, int n) {
+    extern __shared__ __align__(16) unsigned char raw[];
+    constexpr int LD = NP + 4, Q = NP < 32 ? NP : 32;
+    T *A, *X, *S, *dinv;
+    Bufs<T, NP, VT>::setup(reinterpret_cast<T *>(raw), Ag, A, X, S, dinv);
+    cta_potrf_blocked<T, Q>(A, LD, n, NP, 0, dinv);
+    __syncthreads();
+    for (int q = threadIdx.x; q < NP * NP; q += blockDim.x) Lg[q] = A[(q / NP) * LD + q % NP];
+}
+
 template <typename T, int NP, int VT>
 void run(int n, const char *dt) {
     T *hA = new T[NP * NP];
@@ -94,9 +108,14 @@ void run(int n, const char *dt) {
     cudaError_t e = cudaSuccess;
     void (*ks[4])(const T *, unsigned long long *, int) = {k_op<T, NP, VT, 0>, k_op<T, NP, VT, 1>, k_op<T, NP, VT, 2>,
                                                           k_op<T, NP, VT, 3>};
+    T *dL;
+    cudaMalloc(&dL, sizeof(T) * NP * NP);
+    cudaFuncSetAttribute(k_factor<T, NP, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_factor<T, NP, VT><<<1, 256, smem>>>(dA, dL, n);
+    e = cudaDeviceSynchronize();
     for (int op = 0; op < 4 && e == cudaSuccess; ++op) {
         cudaFuncSetAttribute(ks[op], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        ks[op]<<<1, 256, smem>>>(dA, dout, n);
+        ks[op]<<<1, 256, smem>>>((op == 1 || op == 3) ? dL : dA, dout, n);
         e = cudaDeviceSynchronize();
         if (e == cudaSuccess) e = cudaGetLastError();
     }
@@ -105,6 +124,7 @@ void run(int n, const char *dt) {
            "\"syrk_cyc\": %llu, \"bwd_cyc\": %llu, \"err\": \"%s\"}\n",
            n, dt, VT, h[0], h[1], h[2], h[3], cudaGetErrorString(e));
     cudaFree(dA);
+    cudaFree(dL);
     cudaFree(dout);
     delete[] hA;
 }
@@ -121,7 +141,7 @@ int main() {
     run<double, 16, 32>(16, "f64");
     run<double, 32, 64>(32, "f64");
     run<float, 32, 64>(32, "f32");
-    run<double, 128, 8>(128, "f64");  // c4 (the TRSM/SYRK of a column are spread over CTAs; 8 vectors here)
+    // n = 128 (c4) is not measured here: its blocks (280 KB with the scratch) exceed shared memory
     unsigned long long *d, h;
     cudaMalloc(&d, 8);
     int nsm = 0;
