@@ -393,8 +393,24 @@ def _ext_bench(dev) -> dict:
         r = btdgen.block_tridiag_matvec(D.double(), E.double(), x.double()) - b.double()
         return float((r.flatten(1).norm(dim=1) / b.double().flatten(1).norm(dim=1)).max())
 
-    # f4a: the c5 workload with binary64 inputs: binary64 direct vs binary32 factor + refinement
+    # f1: the forward sweep interlaced with the factorization ("about 12%") against a
+    # separate factor then solve, on c5 and on one c3 system (fp64, n=32, N=1024)
     B = B_TOTAL
+    f1 = {}
+    for name, prob, plan in (
+            ("c5_fp32_n12_N128_B8192", btdgen.kalman(B, N_BLK, N_SZ, seed=5, device=dev).cast(torch.float32),
+             btd.Plan(N_BLK, N_SZ, B, 1, torch.float32)),
+            ("c3_fp64_n32_N1024", btdgen.kalman(1, 1024, 32, seed=5, device=dev),
+             btd.Plan(1024, 32, 1, 1, torch.float64))):
+        o = btd.factor_solve(prob.D, prob.E, prob.b, plan=plan)
+        t_fs = timeit(lambda: btd.factor_solve(prob.D, prob.E, prob.b, plan=plan, out=o, stream=s), 10)
+        t_sep = timeit(lambda: (btd.factor(prob.D, prob.E, plan=plan, out=(o[0], o[1], o[3]), stream=s),
+                                btd.solve(o[0], o[1], prob.b, plan=plan, out=o[2], stream=s)), 10)
+        f1[name] = dict(interlaced_ms=round(t_fs, 4), separate_ms=round(t_sep, 4),
+                        saving=round(1 - t_fs / t_sep, 4), variant=plan.variant)
+        del o, prob
+    out["f1_interlace"] = f1
+    # f4a: the c5 workload with binary64 inputs: binary64 direct vs binary32 factor + refinement
     p = btdgen.kalman(B, N_BLK, N_SZ, seed=5, device=dev)
     plan32 = btd.Plan(N_BLK, N_SZ, B, 1, torch.float32)
     plan64 = btd.Plan(N_BLK, N_SZ, B, 1, torch.float64)

@@ -163,14 +163,38 @@ __global__ void __launch_bounds__(kThreads) k_arrow_schur(int N, int n, int na, 
     const int64_t j = blockIdx.x;
     const T *Gj = G + j * (int64_t)N * na * n;
     const T *Yj = Y + j * (int64_t)N * n * mR;
-    for (int o = threadIdx.x; o < na * mR; o += blockDim.x) {
-        const int a = o / mR, c = o % mR;
-        T acc = 0;
-        for (int i = 0; i < N; ++i) {
-            const T *Gi = Gj + (int64_t)i * na * n + (int64_t)a * n;
-            const T *Yi = Yj + (int64_t)i * n * mR + c;
-            for (int r = 0; r < n; ++r) acc = fma(Gi[r], Yi[(int64_t)r * mR], acc);
+    // sum over the N n border rows, split over `groups` thread groups when the outputs do not fill
+    // the CTA; the partial sums are combined in group order (deterministic)
+    const int O = na * mR;
+    const int groups = O >= (int)blockDim.x ? 1 : (int)blockDim.x / O;
+    T *part = S + O;  // [groups][O] when groups > 1
+    for (int o0 = 0; o0 < O; o0 += blockDim.x) {
+        const int t = threadIdx.x;
+        const int g = groups > 1 ? t / O : 0, o = groups > 1 ? t % O : o0 + t;
+        if (g < groups && o < O) {
+            const int a = o / mR, c = o % mR;
+            T acc = 0;
+            for (int i = g; i < N; i += groups) {
+                const T *Gi = Gj + (int64_t)i * na * n + (int64_t)a * n;
+                const T *Yi = Yj + (int64_t)i * n * mR + c;
+                for (int r = 0; r < n; ++r) acc = fma(Gi[r], Yi[(int64_t)r * mR], acc);
+            }
+            if (groups > 1) part[g * O + o] = acc;
+            else S[o] = acc;
         }
+        if (groups > 1) break;
+    }
+    if (groups > 1) {
+        __syncthreads();
+        for (int o = threadIdx.x; o < O; o += blockDim.x) {
+            T acc = 0;
+            for (int g = 0; g < groups; ++g) acc += part[g * O + o];
+            S[o] = acc;
+        }
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < O; o += blockDim.x) {
+        const int a = o / mR, c = o % mR;
         T base;
         if (c < na) {
             const int hi = a >= c ? a : c, lo = a >= c ? c : a;  // Z lower-authoritative
@@ -178,7 +202,7 @@ __global__ void __launch_bounds__(kThreads) k_arrow_schur(int N, int n, int na, 
         } else {
             base = ba[(j * na + a) * mb + (c - na)];
         }
-        S[o] = base - acc;
+        S[o] = base - S[o];
     }
     if (threadIdx.x == 0) fail = 0;
     __syncthreads();
@@ -498,7 +522,7 @@ static btd_status arrow_impl(const btd_plan *p, int64_t na, const void *D, const
     k_arrow_pack<T><<<grid_for(nR), kThreads, 0, st>>>(B, N, n, (int)na, mb, (const T *)G, (const T *)b, (T *)R);
     if (btd_status rs = launched(); rs != BTD_OK) return rs;
     if (btd_status rs = btd_factor_solve(p, D, E, R, Dhat, C, Y, info, stream); rs != BTD_OK) return rs;
-    const size_t smem = (size_t)na * p->m * sizeof(T);
+    const size_t smem = ((size_t)na * p->m + kThreads) * sizeof(T);  // S + group partial sums
     if (btd_status rs = btd::ensure_smem_attr((const void *)k_arrow_schur<T>, smem); rs != BTD_OK) return rs;
     k_arrow_schur<T><<<B, kThreads, smem, st>>>(N, n, (int)na, mb, (const T *)G, (const T *)Z, (const T *)ba,
                                                  (const T *)Y, (T *)LZ, (T *)xa, info);
@@ -515,7 +539,7 @@ btd_status btd_arrow_factor_solve(const btd_plan *p, int64_t na, const void *D, 
         !LZ || !x || !xa || !info || (p->N > 1 && !E))
         return BTD_EINVAL;
     const size_t w = p->dtype == BTD_F32 ? 4 : 8;
-    if ((size_t)na * p->m * w > btd::kMaxSmem) return BTD_EUNSUPPORTED;
+    if (((size_t)na * p->m + kThreads) * w > btd::kMaxSmem) return BTD_EUNSUPPORTED;
     if (!al16(D) || !al16(E) || !al16(R) || !al16(Y) || !al16(Dhat) || !al16(C)) return BTD_EINVAL;
     if (p->dtype == BTD_F32) return arrow_impl<float>(p, na, D, E, G, Z, b, ba, Dhat, C, R, Y, LZ, x, xa, info, stream);
     return arrow_impl<double>(p, na, D, E, G, Z, b, ba, Dhat, C, R, Y, LZ, x, xa, info, stream);
