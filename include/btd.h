@@ -172,8 +172,9 @@ btd_status btd_mixed_factor_solve(const btd_plan *plan, const double *D, const d
  * Psi^{-1} [G^T | b] (its first na columns are V = Psi^{-1} G^T); LZ [batch][na][na]
  * = chol(Z - G V) (strict upper zero); x [batch][N][n][mb]; x_a [batch][na][mb].
  * R [batch][N][n][na+mb] is caller workspace. info[j] = N + 1 if the border
- * Schur complement is not positive definite (and Psi was). Needs na*(na+mb)
- * elements of shared memory (<= 227 KB). Launches: 4. */
+ * Schur complement is not positive definite (and Psi was). Needs na*(na+mb)+256
+ * elements of shared memory (<= 227 KB). Runs btd_factor, then btd_solve with
+ * the na+mb right-hand sides. Launches: 5 (+ the core calls' own). */
 btd_status btd_arrow_factor_solve(const btd_plan *plan, int64_t na, const void *D, const void *E, const void *G,
                                   const void *Z, const void *b, const void *ba, void *Dhat, void *C, void *R, void *Y,
                                   void *LZ, void *x, void *xa, int32_t *info, void *stream);

@@ -149,10 +149,31 @@ __global__ void k_arrow_pack(int B, int N, int n, int na, int mb, const T *__res
     }
 }
 
+// Same output, tiled: a CTA owns TB consecutive (system, block) pairs; their G blocks (contiguous in
+// memory) are staged in shared memory with coalesced loads, then R is written in its own order
+// (coalesced), reading G^T from shared memory. The direct kernel above reads G with stride n.
+template <typename T>
+__global__ void k_arrow_pack_tiled(int64_t nblk, int n, int na, int mb, int TB, const T *__restrict__ G,
+                                   const T *__restrict__ b, T *__restrict__ R) {
+    extern __shared__ unsigned char smraw[];
+    T *sG = reinterpret_cast<T *>(smraw);  // [TB][na][n]
+    const int mR = na + mb, gsz = na * n, rsz = n * mR;
+    for (int64_t t0 = (int64_t)blockIdx.x * TB; t0 < nblk; t0 += (int64_t)gridDim.x * TB) {
+        const int tb = (int)(nblk - t0 < TB ? nblk - t0 : TB);
+        __syncthreads();
+        for (int q = threadIdx.x; q < tb * gsz; q += blockDim.x) sG[q] = G[t0 * gsz + q];
+        __syncthreads();
+        for (int q = threadIdx.x; q < tb * rsz; q += blockDim.x) {
+            const int bi = q / rsz, w = q % rsz, r = w / mR, c = w % mR;
+            R[t0 * rsz + q] = c < na ? sG[bi * gsz + c * n + r] : b[((t0 + bi) * n + r) * mb + (c - na)];
+        }
+    }
+}
+
 // One CTA per system: S = Z - sum_i G_i V_i, t = b_a - sum_i G_i u_i with Y_i = [V_i | u_i];
 // L_Z = chol(S) (right-looking, in shared memory); x_a = L_Z^{-T} L_Z^{-1} t.
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_arrow_schur(int N, int n, int na, int mb, const T *__restrict__ G,
+__global__ void __launch_bounds__(kThreads) k_arrow_schur(int N, int n, int na, int mb, int IB, const T *__restrict__ G,
                                                           const T *__restrict__ Z, const T *__restrict__ ba,
                                                           const T *__restrict__ Y, T *__restrict__ LZ,
                                                           T *__restrict__ xa, int32_t *__restrict__ info) {
@@ -168,6 +189,39 @@ __global__ void __launch_bounds__(kThreads) k_arrow_schur(int N, int n, int na, 
     const int O = na * mR;
     const int groups = O >= (int)blockDim.x ? 1 : (int)blockDim.x / O;
     T *part = S + O;  // [groups][O] when groups > 1
+    if (IB > 0) {
+        // staged: chunks of IB blocks of G and Y copied to shared memory with coalesced loads
+        T *sG = part + blockDim.x, *sY = sG + (size_t)IB * na * n;
+        const int t = threadIdx.x;
+        const int g = groups > 1 ? t / O : 0;
+        T acc[4] = {0, 0, 0, 0};  // groups == 1: up to 4 outputs per thread (O <= 4 * blockDim)
+        for (int i0 = 0; i0 < N; i0 += IB) {
+            const int ib = N - i0 < IB ? N - i0 : IB;
+            __syncthreads();
+            for (int q = t; q < ib * na * n; q += blockDim.x) sG[q] = Gj[(int64_t)i0 * na * n + q];
+            for (int q = t; q < ib * n * mR; q += blockDim.x) sY[q] = Yj[(int64_t)i0 * n * mR + q];
+            __syncthreads();
+            for (int u = 0; u < 4; ++u) {
+                const int o = groups > 1 ? t % O : u * blockDim.x + t;
+                if (g >= groups || o >= O || (groups > 1 && u > 0)) break;
+                const int a = o / mR, c = o % mR;
+                T v = acc[u];
+                for (int bi = (groups > 1 ? (g - i0 % groups + groups) % groups : 0); bi < ib;
+                     bi += (groups > 1 ? groups : 1)) {
+                    const T *Gi = sG + (size_t)bi * na * n + (size_t)a * n;
+                    const T *Yi = sY + (size_t)bi * n * mR + c;
+                    for (int r = 0; r < n; ++r) v = fma(Gi[r], Yi[r * mR], v);
+                }
+                acc[u] = v;
+            }
+        }
+        for (int u = 0; u < 4; ++u) {
+            const int o = groups > 1 ? t % O : u * blockDim.x + t;
+            if (g >= groups || o >= O || (groups > 1 && u > 0)) break;
+            if (groups > 1) part[g * O + o] = acc[u];
+            else S[o] = acc[u];
+        }
+    } else {
     for (int o0 = 0; o0 < O; o0 += blockDim.x) {
         const int t = threadIdx.x;
         const int g = groups > 1 ? t / O : 0, o = groups > 1 ? t % O : o0 + t;
@@ -183,6 +237,7 @@ __global__ void __launch_bounds__(kThreads) k_arrow_schur(int N, int n, int na, 
             else S[o] = acc;
         }
         if (groups > 1) break;
+    }
     }
     if (groups > 1) {
         __syncthreads();
@@ -519,12 +574,32 @@ static btd_status arrow_impl(const btd_plan *p, int64_t na, const void *D, const
     cudaStream_t st = (cudaStream_t)stream;
     const int B = (int)p->batch, N = (int)p->N, n = (int)p->n, mb = (int)(p->m - na);
     const int64_t nR = (int64_t)B * N * n * p->m;
-    k_arrow_pack<T><<<grid_for(nR), kThreads, 0, st>>>(B, N, n, (int)na, mb, (const T *)G, (const T *)b, (T *)R);
+    const size_t gblk = (size_t)na * n * sizeof(T);
+    if (gblk <= 16384) {
+        const int TB = (int)(49152 / gblk) < 64 ? (int)(49152 / gblk) : 64;
+        const int64_t nblk = (int64_t)B * N;
+        int64_t grid = (nblk + TB - 1) / TB;
+        if (grid > 148 * 8) grid = 148 * 8;
+        k_arrow_pack_tiled<T><<<(int)grid, kThreads, TB * gblk, st>>>(nblk, n, (int)na, mb, TB, (const T *)G,
+                                                                      (const T *)b, (T *)R);
+    } else {
+        k_arrow_pack<T><<<grid_for(nR), kThreads, 0, st>>>(B, N, n, (int)na, mb, (const T *)G, (const T *)b, (T *)R);
+    }
     if (btd_status rs = launched(); rs != BTD_OK) return rs;
-    if (btd_status rs = btd_factor_solve(p, D, E, R, Dhat, C, Y, info, stream); rs != BTD_OK) return rs;
-    const size_t smem = ((size_t)na * p->m + kThreads) * sizeof(T);  // S + group partial sums
+    // factor, then one solve with the na + mb right-hand sides: with many right-hand sides the
+    // batched fused factor+solve holds all of them in shared memory for the whole factorization
+    // (1 CTA/SM at c5 size, m = 9: 10.3 ms) while the separate calls keep the factor at full
+    // occupancy (c5, m = 9: 1.6 + 4.4 ms; measured in profiles/r02/arrow_exp.txt)
+    if (btd_status rs = btd_factor(p, D, E, Dhat, C, info, stream); rs != BTD_OK) return rs;
+    if (btd_status rs = btd_solve(p, Dhat, C, R, Y, stream); rs != BTD_OK) return rs;
+    // S + group partial sums, then IB staged blocks of G and Y when 4 * 256 threads cover the outputs
+    const size_t base = ((size_t)na * p->m + kThreads) * sizeof(T);
+    const size_t perb = ((size_t)na * n + (size_t)n * p->m) * sizeof(T);
+    int IB = (na * p->m <= 4 * kThreads && base + perb <= 96 * 1024) ? (int)((96 * 1024 - base) / perb) : 0;
+    if (IB > 32) IB = 32;
+    const size_t smem = base + (size_t)IB * perb;
     if (btd_status rs = btd::ensure_smem_attr((const void *)k_arrow_schur<T>, smem); rs != BTD_OK) return rs;
-    k_arrow_schur<T><<<B, kThreads, smem, st>>>(N, n, (int)na, mb, (const T *)G, (const T *)Z, (const T *)ba,
+    k_arrow_schur<T><<<B, kThreads, smem, st>>>(N, n, (int)na, mb, IB, (const T *)G, (const T *)Z, (const T *)ba,
                                                  (const T *)Y, (T *)LZ, (T *)xa, info);
     if (btd_status rs = launched(); rs != BTD_OK) return rs;
     k_arrow_update<T><<<grid_for((int64_t)B * N * n * mb), kThreads, 0, st>>>(B, N, n, (int)na, mb, (const T *)Y,
