@@ -193,8 +193,14 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         return BTD_EUNSUPPORTED;
     }
     if (variant == BTD_VARIANT_AUTO) {
-        // few independent systems with enough level-1 columns to spread over the SMs: latency path
-        const bool wide_ok = NB > 0 && wsm <= kMaxSmem && batch * ((N + 1) / 2) <= 4 * 148 && N >= 16;
+        // few independent systems with enough level-1 columns to spread over the SMs: latency path.
+        // One system: WIDE up to 2048 (fp64) / 1024 (fp32) level-1 columns, where the cooperative
+        // PERSIST kernel takes over; with many right-hand sides (m >= 16, e.g. the partition
+        // chunks' border columns) WIDE whenever the system does not fit FUSED (measured,
+        // profiles/r02/wide_vs_persist.txt: fp64 N = 2048: 615 vs 890 us; m = 65: 1.3 vs 8.9 ms).
+        const long long cols = batch * ((N + 1) / 2);
+        const long long wide_cols = batch > 1 ? 4 * 148 : (f32 ? 1024 : 2048);
+        const bool wide_ok = NB > 0 && wsm <= kMaxSmem && N >= 16 && (cols <= wide_cols || (m >= 16 && !fits));
         p->variant = wide_ok ? BTD_VARIANT_WIDE : fits ? BTD_VARIANT_FUSED : BTD_VARIANT_PERSIST;
         if (p->variant == BTD_VARIANT_PERSIST && NB < 0 && psm > kMaxSmem) {  // e.g. n = 128 fp64 with m >= 32
             delete p;

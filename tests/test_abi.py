@@ -60,7 +60,12 @@ def test_variant_selection():
     # n <= 32 whose column ops fit 4 CTAs per SM -> wide (c2, c3); n > 32 -> persist (c4)
     assert btd.Plan(128, 12, 8192, 1, torch.float32).variant == "fused"
     assert btd.Plan(1024, 32, 1, 1, torch.float64).variant == "wide"
-    assert btd.Plan(4096, 32, 1, 1, torch.float64).variant == "persist"
+    assert btd.Plan(4096, 32, 1, 1, torch.float64).variant == "wide"     # <= 2048 level-1 columns (fp64)
+    assert btd.Plan(8192, 32, 1, 1, torch.float64).variant == "persist"
+    assert btd.Plan(2048, 32, 1, 1, torch.float32).variant == "wide"     # <= 1024 (fp32)
+    assert btd.Plan(4096, 32, 1, 1, torch.float32).variant == "persist"
+    assert btd.Plan(8192, 32, 1, 65, torch.float64).variant == "wide"    # many right-hand sides
+    assert btd.Plan(1000, 32, 4, 1, torch.float64).variant == "persist"  # batched: 4 x 148 columns
     assert btd.Plan(256, 128, 1, 1, torch.float64).variant == "persist"
     assert btd.Plan(64, 16, 1, 1, torch.float64).variant == "wide"
     assert btd.Plan(8, 16, 1, 1, torch.float64).variant == "fused"
@@ -71,7 +76,7 @@ def test_variant_selection():
     with pytest.raises(btd.BtdError):
         btd.Plan(256, 64, 1, 1, torch.float64, variant="level")
     with pytest.raises(btd.BtdError):
-        btd.Plan(4096, 32, 1, 1, torch.float64, variant="fused")
+        btd.Plan(8192, 32, 1, 1, torch.float64, variant="fused")
 
 
 @pytest.mark.parametrize("args", [(0, 4, 1, 1), (4, 0, 1, 1), (4, 4, 0, 1), (4, 4, 1, 0)])

@@ -119,3 +119,25 @@ def test_shard_range():
         shard.shard_range(0, 4, 3)
     one = shard.gather_stats(torch.zeros(6, dtype=torch.float64), 1)
     assert one.shape == (1, 6)
+
+
+def test_critical_path_floor_from_chain_latency(monkeypatch, tmp_path):
+    """bench._critical_path: t_chain(n) from the microbenchmark's JSON lines and the floor
+    L(N) x (t_chain + t_sync) against the measured latency (SURVEY.md §8(d) regime 1)."""
+    import subprocess
+    import types
+
+    lines = ['{"n": 16, "dtype": "f64", "trsm_vectors": 32, "potrf_cyc": 3930, "trsm_cyc": 1965, '
+             '"syrk_cyc": 0, "bwd_cyc": 0, "err": "no error"}',
+             '{"n": 32, "dtype": "f64", "trsm_vectors": 64, "potrf_cyc": 0, "trsm_cyc": 0, "syrk_cyc": 0, '
+             '"bwd_cyc": 0, "err": "too many resources"}',
+             '{"gridsync_cyc": 1965, "grid": 148, "sm_khz": 1965000}']
+    monkeypatch.setattr(bench.os.path, "exists", lambda p: True)
+    monkeypatch.setattr(subprocess, "run", lambda *a, **k: types.SimpleNamespace(stdout="\n".join(lines)))
+    lat = {"c2_fp64_n16": {"64": {"graph_warm": 30.0}}, "c3_fp64_n32": {"1024": {"graph_warm": 400.0}}}
+    out = bench._critical_path(torch.device("cpu"), lat)
+    assert out["gridsync_us"] == 1.0 and out["chain"]["f64_n16"]["chain_us"] == 3.0
+    assert "f64_n32" not in out["chain"]                   # failed rows are dropped
+    f = out["floors"]["c2_fp64_n16/N64"]                     # L(64) = 7 levels x (3 + 1) us
+    assert f["floor_us"] == 28.0 and abs(f["frac"] - 28.0 / 30.0) < 1e-4
+    assert "c3_fp64_n32/N1024" not in out["floors"]
