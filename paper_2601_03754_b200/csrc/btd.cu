@@ -200,7 +200,11 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         // profiles/r02/wide_vs_persist.txt: fp64 N = 2048: 615 vs 890 us; m = 65: 1.3 vs 8.9 ms).
         const long long cols = batch * ((N + 1) / 2);
         const long long wide_cols = batch > 1 ? 4 * 148 : (f32 ? 1024 : 2048);
-        const bool wide_ok = NB > 0 && wsm <= kMaxSmem && N >= 16 && (cols <= wide_cols || (m >= 16 && !fits));
+        // short systems: FUSED (one CTA) wins below 16 blocks except for 32-wide blocks, where one CTA per
+        // column op already pays from N = 4 (fp64) / 12 (fp32) (profiles/r02/small_n.txt: fp64 n = 32,
+        // N = 8: 104 vs 141 us; N = 15: 105 vs 208 us)
+        const bool long_enough = N >= 16 || (NB == 32 && N >= (f32 ? 12 : 4));
+        const bool wide_ok = NB > 0 && wsm <= kMaxSmem && long_enough && (cols <= wide_cols || (m >= 16 && !fits));
         p->variant = wide_ok ? BTD_VARIANT_WIDE : fits ? BTD_VARIANT_FUSED : BTD_VARIANT_PERSIST;
         if (p->variant == BTD_VARIANT_PERSIST && NB < 0 && psm > kMaxSmem) {  // e.g. n = 128 fp64 with m >= 32
             delete p;

@@ -325,3 +325,12 @@ def test_config_c5_batched_fp32_n12_N128():
         r = btdgen.block_tridiag_matvec(Dd, Ed, xd) - bd
         rel = r.flatten(1).norm(dim=1) / bd.flatten(1).norm(dim=1)
         assert float(rel.max()) <= 1e-5, float(rel.max())
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_auto_short_systems_with_32_wide_blocks(dtype):
+    """AUTO picks WIDE for short single systems with n = 32 (N >= 4 fp64, N >= 12 fp32) and for
+    long ones up to 2048 / 1024 level-1 columns: parity at the switch points."""
+    for N in (2, 3, 4, 5, 8, 11, 12, 15, 2047, 2049):
+        prob = btdgen.kalman(1, N, 32, m=1, seed=N)
+        _check(*_run(prob, dtype, "auto"), dtype, check_L=N < 1000)
