@@ -183,3 +183,24 @@ def test_partition_parity(dtype, N, n, p, rule):
         # and its factor is the nested-dissection factor of that system (O3)
         Do, Co = ndchol.factor(np.stack(ref["S_diag"]), np.stack(ref["S_off"]) if p > 2 else np.zeros((0, n, n)))
         assert metrics.err_L(red["DhatS"].cpu().double().numpy(), red["CS"].cpu().double().numpy(), Do, Co) <= tol["L"]
+
+
+def test_extension_failure_reporting():
+    """A non-SPD block is reported through info by every extension path (LAPACK style)."""
+    dev = _dev()
+    # mixed: the binary32 pivot of block 5 of system 1 fails
+    prob = btdgen.dd(3, 16, 4, seed=2)
+    prob.D[1, 4] = -prob.D[1, 4]
+    info = ext.mixed_factor_solve(prob.D.to(dev), prob.E.to(dev), prob.b.to(dev), iters=1)[3].cpu()
+    assert info[0] == 0 and info[2] == 0 and info[1] != 0
+    # banded: a failing super-block pivot
+    q = btdgen.banded(2, 12, 2, 3, seed=3)
+    q.D[0, 7] = -q.D[0, 7]
+    t = q.to(dev)
+    info = ext.banded_factor_solve(t.D, t.A, t.b)[3].cpu()
+    assert info[0] != 0 and info[1] == 0
+    # partition: a failing chunk block shows up in that chunk's info
+    p = btdgen.dd(1, 40, 3, seed=4)
+    p.D[0, 2] = -p.D[0, 2]
+    _, st = part.solve(p.D[0].to(dev), p.E[0].to(dev), p.b[0].to(dev), 3)
+    assert sum(int(i.abs().sum()) != 0 for i in st["info"]) >= 1
