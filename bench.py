@@ -455,6 +455,31 @@ def _ext_bench(dev) -> dict:
 
 # ------------------------------------------------------------------ the batched benchmark, one rank
 
+def _pcie_bandwidth(dev, mb: int = 512) -> dict | None:
+    """Pinned host <-> device copy bandwidth (GB/s), each direction alone: best of 5 copies of
+    `mb` MB, CUDA events. The ceiling of the e2e number (all step bytes cross PCIe)."""
+    try:
+        h = torch.empty(mb << 20, dtype=torch.uint8, pin_memory=True)
+        d = torch.empty(mb << 20, dtype=torch.uint8, device=dev)
+        s = torch.cuda.Stream(dev)
+        out = {}
+        for name, dst, src in (("h2d_gbs", d, h), ("d2h_gbs", h, d)):
+            best = 0.0
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(s):
+                    e0.record(s)
+                    dst.copy_(src, non_blocking=True)
+                    e1.record(s)
+                e1.synchronize()
+                best = max(best, (mb << 20) / (e0.elapsed_time(e1) / 1e3) / 1e9)
+            out[name] = best
+        out["how"] = f"pinned {mb} MB copy each direction alone, best of 5, CUDA events"
+        return out
+    except Exception:
+        return None
+
+
 class _CudaClock:
     """Device time with CUDA events on the launching stream."""
 
@@ -567,7 +592,7 @@ def run_rank(args, rank: int, world: int, dev: torch.device, step_factory=None, 
         stream.synchronize()
         h2d = (hD.numel() + hE.numel() + hb.numel()) * W_BYTES
         d2h = (Dhat.numel() + C.numel() + x.numel()) * W_BYTES + info.numel() * 4
-        e2e = dict(t=clock.ms(e0, e1) / 1e3, steps=args.e2e_steps, h2d=h2d, d2h=d2h)
+        e2e = dict(t=clock.ms(e0, e1) / 1e3, steps=args.e2e_steps, h2d=h2d, d2h=d2h, pcie=_pcie_bandwidth(dev))
         del ws_h
 
     stats = torch.tensor([t_total, statistics.mean(kern_ms), rel, float(nfail), e2e["t"] if e2e else 0.0,
@@ -617,6 +642,14 @@ def build_line(args, agg: dict, local: dict, pk: dict | None = None) -> dict:
                        "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"],
                        "chunks": args.e2e_chunks,
                        "api": "btd_factor_solve_host (pinned host buffers, copies inside the timed region)"}
+        pc = e2e.get("pcie")
+        if pc:
+            # the copies of one step overlap each other and the kernels: the slower direction bounds it
+            floor_s = max(e2e["h2d"] / (pc["h2d_gbs"] * 1e9), e2e["d2h"] / (pc["d2h_gbs"] * 1e9))
+            line["e2e"]["roofline"] = {"bound": "pcie", "h2d_gbs": pc["h2d_gbs"], "d2h_gbs": pc["d2h_gbs"],
+                                       "ceiling": per_step / floor_s,
+                                       "frac": line["e2e"]["value"] / (per_step / floor_s),
+                                       "how": pc["how"]}
     return line
 
 
