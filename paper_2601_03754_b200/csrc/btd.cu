@@ -54,6 +54,15 @@ static bool al4(const void *p) { return ((uintptr_t)p & 3u) == 0; }
 
 static const int kSizes[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
 
+// Largest N for which ONE system runs faster in the one-CTA FUSED kernel (no grid barriers) than in
+// the cooperative WIDE kernel, per dtype and compiled block size (measured on B200,
+// profiles/r02/fused_vs_wide_single.txt; e.g. fp64 n = 4, N = 64: 23 vs 73 us; n = 12: FUSED up to
+// N = 64, WIDE from 128; n = 16: FUSED only at N = 16).
+static int64_t fused_max_n_single(bool f32, int NB) {
+    if (f32) return NB <= 8 ? 1024 : NB <= 12 ? 128 : NB <= 16 ? 64 : NB <= 24 ? 16 : 11;
+    return NB <= 4 ? 1024 : NB <= 8 ? 192 : NB <= 12 ? 96 : NB <= 24 ? 16 : 3;
+}
+
 static int pick_nb(int64_t n) {
     for (int s : kSizes)
         if (n <= s) return s;
@@ -205,7 +214,9 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         // N = 8: 104 vs 141 us; N = 15: 105 vs 208 us)
         const bool long_enough = N >= 16 || (NB == 32 && N >= (f32 ? 12 : 4));
         const bool wide_ok = NB > 0 && wsm <= kMaxSmem && long_enough && (cols <= wide_cols || (m >= 16 && !fits));
-        p->variant = wide_ok ? BTD_VARIANT_WIDE : fits ? BTD_VARIANT_FUSED : BTD_VARIANT_PERSIST;
+        const bool fused_first = batch == 1 && fits && N <= fused_max_n_single(f32, NB);
+        p->variant = fused_first ? BTD_VARIANT_FUSED : wide_ok ? BTD_VARIANT_WIDE : fits ? BTD_VARIANT_FUSED
+                                                                                      : BTD_VARIANT_PERSIST;
         if (p->variant == BTD_VARIANT_PERSIST && NB < 0 && psm > kMaxSmem) {  // e.g. n = 128 fp64 with m >= 32
             delete p;
             return BTD_EUNSUPPORTED;

@@ -72,6 +72,11 @@ def test_variant_selection():
     assert btd.Plan(8, 32, 1, 1, torch.float64).variant == "wide"       # 32-wide blocks: from N = 4 (fp64)
     assert btd.Plan(8, 32, 1, 1, torch.float32).variant == "fused"      # ... and N = 12 (fp32)
     assert btd.Plan(12, 32, 1, 1, torch.float32).variant == "wide"
+    # one short system with small blocks: the one-CTA FUSED kernel (no grid barriers) wins
+    assert btd.Plan(512, 4, 1, 1, torch.float64).variant == "fused"
+    assert btd.Plan(64, 12, 1, 1, torch.float64).variant == "fused"
+    assert btd.Plan(128, 12, 1, 1, torch.float64).variant == "wide"
+    assert btd.Plan(128, 12, 1, 1, torch.float32).variant == "fused"
     assert btd.Plan(8, 2, 1, 1, torch.float64).launches() == 1
     assert btd.Plan(1024, 32, 1, 1, torch.float64).launches() == 1
     p = btd.Plan(1024, 32, 1, 1, torch.float64, variant="level")
