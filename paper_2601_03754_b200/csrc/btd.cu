@@ -214,7 +214,8 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         // N = 8: 104 vs 141 us; N = 15: 105 vs 208 us)
         const bool long_enough = N >= 16 || (NB == 32 && N >= (f32 ? 12 : 4));
         const bool wide_ok = NB > 0 && wsm <= kMaxSmem && long_enough && (cols <= wide_cols || (m >= 16 && !fits));
-        const bool fused_first = batch == 1 && fits && N <= fused_max_n_single(f32, NB);
+        // up to one system per SM the FUSED CTAs all run at once: the single-system crossover applies
+        const bool fused_first = batch <= 148 && fits && N <= fused_max_n_single(f32, NB);
         p->variant = fused_first ? BTD_VARIANT_FUSED : wide_ok ? BTD_VARIANT_WIDE : fits ? BTD_VARIANT_FUSED
                                                                                       : BTD_VARIANT_PERSIST;
         if (p->variant == BTD_VARIANT_PERSIST && NB < 0 && psm > kMaxSmem) {  // e.g. n = 128 fp64 with m >= 32

@@ -77,6 +77,8 @@ def test_variant_selection():
     assert btd.Plan(64, 12, 1, 1, torch.float64).variant == "fused"
     assert btd.Plan(128, 12, 1, 1, torch.float64).variant == "wide"
     assert btd.Plan(128, 12, 1, 1, torch.float32).variant == "fused"
+    assert btd.Plan(128, 12, 8, 1, torch.float32).variant == "fused"      # <= 148 systems: all CTAs at once
+    assert btd.Plan(128, 16, 4, 1, torch.float64).variant == "wide"
     assert btd.Plan(8, 2, 1, 1, torch.float64).launches() == 1
     assert btd.Plan(1024, 32, 1, 1, torch.float64).launches() == 1
     p = btd.Plan(1024, 32, 1, 1, torch.float64, variant="level")
