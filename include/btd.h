@@ -161,6 +161,12 @@ btd_status btd_mixed_workspace_bytes(const btd_plan *plan, size_t *bytes);
 btd_status btd_mixed_factor_solve(const btd_plan *plan, const double *D, const double *E, const double *b,
                                   float *Dhat, float *C, double *x, int32_t *info, int32_t iters, double *resid,
                                   void *work, void *stream);
+/* The same refinement for a new right-hand side with a binary32 factor (Dhat, C) from
+ * btd_mixed_factor_solve (or btd_factor on fl32(D, E)): x_0 = solve32(fl32(b)), then iters
+ * steps with the binary64 residual of (D, E). Same workspace. Launches: 2 + 2*iters + 1. */
+btd_status btd_mixed_solve(const btd_plan *plan, const double *D, const double *E, const double *b,
+                           const float *Dhat, const float *C, double *x, int32_t iters, double *resid, void *work,
+                           void *stream);
 
 /* f4b arrowhead ("arrow structures"; R9): solves
  *   [[Psi, G^T], [G, Z]] [x; x_a] = [b; b_a]

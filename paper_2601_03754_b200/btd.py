@@ -47,6 +47,7 @@ SIGNATURES = [
     ("btd_factor_solve_host", ctypes.c_int, [_vp] * 15 + [_i32, _vp]),
     ("btd_mixed_workspace_bytes", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_size_t)]),
     ("btd_mixed_factor_solve", ctypes.c_int, [_vp] * 8 + [_i32, _vp, _vp, _vp]),
+    ("btd_mixed_solve", ctypes.c_int, [_vp] * 7 + [_i32, _vp, _vp, _vp]),
     ("btd_arrow_factor_solve", ctypes.c_int, [_vp, _i64] + [_vp] * 15),
     ("btd_banded_factor_solve", ctypes.c_int, [_vp, _i64, _i64, _i64] + [_vp] * 12),
     ("btd_partition_local", ctypes.c_int, [_vp] * 15),

@@ -515,27 +515,14 @@ btd_status btd_mixed_workspace_bytes(const btd_plan *p, size_t *bytes) {
     return BTD_OK;
 }
 
-btd_status btd_mixed_factor_solve(const btd_plan *p, const double *D, const double *E, const double *b,
-                                  float *Dhat, float *C, double *x, int32_t *info, int32_t iters, double *resid,
-                                  void *work, void *stream) {
-    if (!p || p->dtype != BTD_F32 || !D || !b || !Dhat || (!C && p->geo.nC > 0) || !x || !info || !work ||
-        iters < 0 || (p->N > 1 && !E))
-        return BTD_EINVAL;
-    if (!al16(D) || !al16(E) || !al16(b) || !al16(x) || !al16(work)) return BTD_EINVAL;
+// The refinement loop shared by btd_mixed_factor_solve and btd_mixed_solve: on entry w.d32 holds
+// x_0 = solve32(fl32(b)); x_j for j = 0..iters alternates buffers so that x_iters lands in x.
+static btd_status mixed_refine(const btd_plan *p, const double *D, const double *E, const double *b,
+                               const float *Dhat, const float *C, double *x, int32_t iters, double *resid,
+                               const MixedWs &w, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    MixedWs w;
-    mixed_layout(p, (char *)work, &w);
     const int B = (int)p->batch, N = (int)p->N, n = (int)p->n, m = (int)p->m;
-    const int64_t nn = (int64_t)n * n, nx = (int64_t)B * N * n * m;
-    k_demote<<<grid_for((int64_t)B * N * nn / 2), kThreads, 0, st>>>(D, w.D32, (int64_t)B * N * nn);
-    if (N > 1) k_demote<<<grid_for((int64_t)B * (N - 1) * nn / 2), kThreads, 0, st>>>(E, w.E32, (int64_t)B * (N - 1) * nn);
-    k_demote<<<grid_for(nx / 2), kThreads, 0, st>>>(b, w.r32, nx);
-    if (btd_status rs = launched(); rs != BTD_OK) return rs;
-    // x_0 = solve32(fl32(b)), then iters x (x_k = x_{k-1} + d_k, r = b - Psi x_k, d = solve32(r)).
-    if (btd_status rs = btd_factor_solve(p, w.D32, N > 1 ? w.E32 : nullptr, w.r32, Dhat, C, w.d32, info, stream);
-        rs != BTD_OK)
-        return rs;
-    // x_j for j = 0..iters alternates buffers so that x_iters lands in the caller's x
+    const int64_t nx = (int64_t)B * N * n * m;
     auto xbuf = [&](int j) { return ((iters - j) % 2 == 0) ? x : w.xtmp; };
     const int g = grid_for(nx);
     for (int k = 0; k <= iters; ++k) {
@@ -565,6 +552,45 @@ btd_status btd_mixed_factor_solve(const btd_plan *p, const double *D, const doub
         }
     }
     return launched();
+}
+
+btd_status btd_mixed_factor_solve(const btd_plan *p, const double *D, const double *E, const double *b,
+                                  float *Dhat, float *C, double *x, int32_t *info, int32_t iters, double *resid,
+                                  void *work, void *stream) {
+    if (!p || p->dtype != BTD_F32 || !D || !b || !Dhat || (!C && p->geo.nC > 0) || !x || !info || !work ||
+        iters < 0 || (p->N > 1 && !E))
+        return BTD_EINVAL;
+    if (!al16(D) || !al16(E) || !al16(b) || !al16(x) || !al16(work)) return BTD_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    MixedWs w;
+    mixed_layout(p, (char *)work, &w);
+    const int B = (int)p->batch, N = (int)p->N, n = (int)p->n, m = (int)p->m;
+    const int64_t nn = (int64_t)n * n, nx = (int64_t)B * N * n * m;
+    k_demote<<<grid_for((int64_t)B * N * nn / 2), kThreads, 0, st>>>(D, w.D32, (int64_t)B * N * nn);
+    if (N > 1) k_demote<<<grid_for((int64_t)B * (N - 1) * nn / 2), kThreads, 0, st>>>(E, w.E32, (int64_t)B * (N - 1) * nn);
+    k_demote<<<grid_for(nx / 2), kThreads, 0, st>>>(b, w.r32, nx);
+    if (btd_status rs = launched(); rs != BTD_OK) return rs;
+    // x_0 = solve32(fl32(b)), then iters x (x_k = x_{k-1} + d_k, r = b - Psi x_k, d = solve32(r)).
+    if (btd_status rs = btd_factor_solve(p, w.D32, N > 1 ? w.E32 : nullptr, w.r32, Dhat, C, w.d32, info, stream);
+        rs != BTD_OK)
+        return rs;
+    return mixed_refine(p, D, E, b, Dhat, C, x, iters, resid, w, stream);
+}
+
+btd_status btd_mixed_solve(const btd_plan *p, const double *D, const double *E, const double *b, const float *Dhat,
+                           const float *C, double *x, int32_t iters, double *resid, void *work, void *stream) {
+    if (!p || p->dtype != BTD_F32 || !D || !b || !Dhat || (!C && p->geo.nC > 0) || !x || !work || iters < 0 ||
+        (p->N > 1 && !E))
+        return BTD_EINVAL;
+    if (!al16(D) || !al16(E) || !al16(b) || !al16(x) || !al16(work) || !al16(Dhat) || !al16(C)) return BTD_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    MixedWs w;
+    mixed_layout(p, (char *)work, &w);
+    const int64_t nx = (int64_t)p->batch * p->N * p->n * p->m;
+    k_demote<<<grid_for(nx / 2), kThreads, 0, st>>>(b, w.r32, nx);
+    if (btd_status rs = launched(); rs != BTD_OK) return rs;
+    if (btd_status rs = btd_solve(p, Dhat, C, w.r32, w.d32, stream); rs != BTD_OK) return rs;
+    return mixed_refine(p, D, E, b, Dhat, C, x, iters, resid, w, stream);
 }
 
 template <typename T>

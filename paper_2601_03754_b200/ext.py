@@ -1,6 +1,7 @@
 """Bindings of the §8(f) extension entry points of include/btd.h (argument marshalling only).
 
 * ``mixed_factor_solve``  -- btd_mixed_factor_solve: binary32 factor + binary64 iterative refinement.
+* ``mixed_solve``         -- btd_mixed_solve: the refinement for a new right-hand side, same factor.
 * ``arrow_factor_solve``  -- btd_arrow_factor_solve: block-tridiagonal-arrow systems.
 * ``banded_factor_solve`` -- btd_banded_factor_solve: block-banded systems (bandwidth w).
 
@@ -52,6 +53,38 @@ def mixed_factor_solve(D: torch.Tensor, E: torch.Tensor, b: torch.Tensor, iters:
                                             _ptr(C), _ptr(x), _ptr(info), int(iters), _ptr(resid), _ptr(work),
                                             _stream(stream, dev)), "btd_mixed_factor_solve")
     return Dhat, C, x, info, resid
+
+
+def mixed_solve(D: torch.Tensor, E: torch.Tensor, b: torch.Tensor, Dhat: torch.Tensor, C: torch.Tensor,
+                iters: int = 3, plan: Plan | None = None, want_resid: bool = False, stream=None,
+                work: torch.Tensor | None = None):
+    """btd_mixed_solve: refinement for a new binary64 b with the binary32 factor (Dhat, C) of
+    mixed_factor_solve -> (x64, resid64 | None)."""
+    B, N, n, _ = D.shape
+    m = b.shape[3]
+    if plan is None:
+        plan = Plan(N, n, B, m, torch.float32)
+    if plan.dtype != torch.float32 or (plan.batch, plan.N, plan.n, plan.m) != (B, N, n, m):
+        raise ValueError("mixed_solve needs a float32 plan of the system's shape")
+    sh = _shapes(plan)
+    dev = D.device
+    _check_in("D", D, sh["D"], torch.float64, dev)
+    _check_in("E", E, sh["E"], torch.float64, dev)
+    _check_in("b", b, sh["b"], torch.float64, dev)
+    _check_in("Dhat", Dhat, sh["D"], torch.float32, dev)
+    _check_in("C", C, sh["C"], torch.float32, dev)
+    x = torch.empty(sh["b"], dtype=torch.float64, device=dev)
+    resid = torch.empty(B, dtype=torch.float64, device=dev) if want_resid else None
+    nbytes = mixed_workspace_bytes(plan)
+    if work is None:
+        work = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    elif work.numel() < nbytes or not work.is_cuda or work.data_ptr() % 16:
+        raise ValueError(f"work must be a 16-byte aligned device buffer of >= {nbytes} bytes")
+    with torch.cuda.device(dev):
+        _check(lib().btd_mixed_solve(plan.handle, _ptr(D), _ptr(E) if N > 1 else None, _ptr(b), _ptr(Dhat), _ptr(C),
+                                     _ptr(x), int(iters), _ptr(resid), _ptr(work), _stream(stream, dev)),
+               "btd_mixed_solve")
+    return x, resid
 
 
 def arrow_factor_solve(D, E, G, Z, b, ba, plan: Plan | None = None, stream=None):

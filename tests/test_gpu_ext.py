@@ -81,6 +81,28 @@ def test_mixed_zero_iterations_is_the_binary32_path():
         assert 1e-9 < r < 1e-5 and abs(float(res0[j]) - r) <= 1e-6 * r
 
 
+def test_mixed_solve_reuses_the_binary32_factor():
+    """btd_mixed_solve with the factor of btd_mixed_factor_solve reaches the binary64 solution of a
+    NEW right-hand side, and agrees with the factor+solve result for the same b (x_0 comes from the
+    solve-only kernel instead of the interlaced one: equal to binary64 rounding, not bitwise)."""
+    dev = _dev()
+    prob = btdgen.kalman(5, 64, 12, m=2, seed=31)
+    D, E, b = prob.D.to(dev), prob.E.to(dev), prob.b.to(dev)
+    Dh, C, x1, info, _ = ext.mixed_factor_solve(D, E, b, iters=3)
+    x2, _ = ext.mixed_solve(D, E, b, Dh, C, iters=3)
+    torch.cuda.synchronize()
+    assert int(info.abs().sum()) == 0
+    assert float((x1 - x2).abs().max() / x1.abs().max()) <= 1e-13
+    b2 = torch.randn_like(b)
+    x3, res = ext.mixed_solve(D, E, b2, Dh, C, iters=4, want_resid=True)
+    torch.cuda.synchronize()
+    for j in (0, 4):
+        Dj, Ej = prob.D[j].numpy(), prob.E[j].numpy()
+        bj = b2[j].cpu().numpy()
+        assert metrics.err_x(x3[j].cpu().numpy(), _o1(Dj, Ej, bj)) <= 1e-10
+        assert metrics.residual(Dj, Ej, x3[j].cpu().numpy(), bj) <= 1e-12 and float(res[j]) <= 1e-12
+
+
 def test_mixed_error_contracts_per_iteration():
     dev = _dev()
     prob = btdgen.kalman(2, 128, 12, seed=21)
