@@ -474,7 +474,26 @@ def _pcie_bandwidth(dev, mb: int = 512) -> dict | None:
                 e1.synchronize()
                 best = max(best, (mb << 20) / (e0.elapsed_time(e1) / 1e3) / 1e9)
             out[name] = best
-        out["how"] = f"pinned {mb} MB copy each direction alone, best of 5, CUDA events"
+        # both directions at once (separate streams and buffers): the bidirectional rate
+        h2, d2 = torch.empty_like(h), torch.empty_like(d)
+        s2 = torch.cuda.Stream(dev)
+        best = 0.0
+        for _ in range(5):
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            s2.wait_event(e0)
+            with torch.cuda.stream(s):
+                d.copy_(h, non_blocking=True)
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+            s.wait_stream(s2)
+            e1.record(s)
+            e1.synchronize()
+            best = max(best, 2 * (mb << 20) / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        out["bidir_gbs"] = best
+        out["how"] = (f"pinned {mb} MB copies, each direction alone and both at once on two streams, best of 5, "
+                      f"CUDA events")
         return out
     except Exception:
         return None
@@ -644,9 +663,12 @@ def build_line(args, agg: dict, local: dict, pk: dict | None = None) -> dict:
                        "api": "btd_factor_solve_host (pinned host buffers, copies inside the timed region)"}
         pc = e2e.get("pcie")
         if pc:
-            # the copies of one step overlap each other and the kernels: the slower direction bounds it
-            floor_s = max(e2e["h2d"] / (pc["h2d_gbs"] * 1e9), e2e["d2h"] / (pc["d2h_gbs"] * 1e9))
+            # the copies of one step overlap each other and the kernels: the slower direction, or both
+            # directions together, bound it
+            floor_s = max(e2e["h2d"] / (pc["h2d_gbs"] * 1e9), e2e["d2h"] / (pc["d2h_gbs"] * 1e9),
+                          (e2e["h2d"] + e2e["d2h"]) / (pc.get("bidir_gbs", float("inf")) * 1e9))
             line["e2e"]["roofline"] = {"bound": "pcie", "h2d_gbs": pc["h2d_gbs"], "d2h_gbs": pc["d2h_gbs"],
+                                       "bidir_gbs": pc.get("bidir_gbs"),
                                        "ceiling": per_step / floor_s,
                                        "frac": line["e2e"]["value"] / (per_step / floor_s),
                                        "how": pc["how"]}
