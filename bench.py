@@ -475,7 +475,8 @@ def _pcie_bandwidth(dev, mb: int = 512) -> dict | None:
                 best = max(best, (mb << 20) / (e0.elapsed_time(e1) / 1e3) / 1e9)
             out[name] = best
         # both directions at once (separate streams and buffers): the bidirectional rate
-        h2, d2 = torch.empty_like(h), torch.empty_like(d)
+        h2 = torch.empty(mb << 20, dtype=torch.uint8, pin_memory=True)  # empty_like drops pinning
+        d2 = torch.empty_like(d)
         s2 = torch.cuda.Stream(dev)
         best = 0.0
         for _ in range(5):
