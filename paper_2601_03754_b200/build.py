@@ -30,6 +30,13 @@ def _nvcc() -> str:
     return "nvcc"
 
 
+def _nvcc_path() -> str:
+    import shutil
+
+    c = _nvcc()
+    return c if os.path.isabs(c) else (shutil.which(c) or "/usr/local/cuda/bin/nvcc")
+
+
 def _sources() -> list[str]:
     out = [os.path.join(ROOT, "include", "btd.h")]
     for f in os.listdir(CSRC):
@@ -104,6 +111,20 @@ def build_micro(name: str) -> str:
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     if _stale(exe, deps):
         subprocess.run([_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-o", exe, src], check=True)
+    return exe
+
+
+def build_c_demo() -> str:
+    """tools/c_api_demo: the C ABI used from plain C, linked against the in-tree libbtd.so."""
+    src = os.path.join(ROOT, "tools", "c_api_demo.c")
+    exe = os.path.join(ROOT, "tools", "c_api_demo")
+    if _stale(exe, [src, LIB, os.path.join(ROOT, "include", "btd.h")]):
+        cuda = os.path.dirname(os.path.dirname(os.path.realpath(_nvcc_path())))
+        # plain C (gcc -std=c11): the header and the library are usable without any C++ or CUDA compiler
+        subprocess.run(["gcc", "-std=c11", "-O2", "-o", exe, src, "-I" + os.path.join(ROOT, "include"),
+                        "-I" + os.path.join(cuda, "include"), "-L" + HERE, "-lbtd",
+                        "-L" + os.path.join(cuda, "lib64"), "-lcudart", "-lm",
+                        "-Wl,-rpath," + HERE + ":" + os.path.join(cuda, "lib64")], check=True)
     return exe
 
 

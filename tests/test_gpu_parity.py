@@ -334,3 +334,17 @@ def test_auto_short_systems_with_32_wide_blocks(dtype):
     for N in (2, 3, 4, 5, 8, 11, 12, 15, 2047, 2049):
         prob = btdgen.kalman(1, N, 32, m=1, seed=N)
         _check(*_run(prob, dtype, "auto"), dtype, check_L=N < 1000)
+
+
+def test_c_abi_from_plain_c():
+    """tools/c_api_demo.c (gcc -std=c11, no Python/torch): plan, cudaMalloc'd buffers, btd_factor_solve,
+    known solution -- the boundary is usable from C as include/btd.h documents it."""
+    import subprocess
+
+    _dev()
+    from paper_2601_03754_b200 import build
+
+    exe = build.build_c_demo()
+    for args in ([], ["1", "3"], ["1000", "32"], ["37", "12"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0 and "c_api_demo ok" in r.stdout, (args, r.stdout, r.stderr)
