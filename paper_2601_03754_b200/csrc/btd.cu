@@ -208,7 +208,10 @@ btd_status btd_plan_create_ex(btd_plan **out, int64_t N, int64_t n, int64_t batc
         // chunks' border columns) WIDE whenever the system does not fit FUSED (measured,
         // profiles/r02/wide_vs_persist.txt: fp64 N = 2048: 615 vs 890 us; m = 65: 1.3 vs 8.9 ms).
         const long long cols = batch * ((N + 1) / 2);
-        const long long wide_cols = batch > 1 ? 4 * 148 : (f32 ? 1024 : 2048);
+        // several long systems: the single-system crossover holds for fp64 n = 32 (WIDE's DMMA tiles),
+        // PERSIST wins the others (profiles/r02/wide_vs_persist_batched.txt: 4 x fp64 N = 512 n = 32:
+        // 535 vs 775 us; 4 x fp64 N = 1024 n = 16: 407 vs 312 us)
+        const long long wide_cols = batch > 1 ? ((!f32 && NB == 32) ? 2048 : 4 * 148) : (f32 ? 1024 : 2048);
         // short systems: FUSED (one CTA) wins below 16 blocks except for 32-wide blocks, where one CTA per
         // column op already pays from N = 4 (fp64) / 12 (fp32) (profiles/r02/small_n.txt: fp64 n = 32,
         // N = 8: 104 vs 141 us; N = 15: 105 vs 208 us)

@@ -65,7 +65,9 @@ def test_variant_selection():
     assert btd.Plan(2048, 32, 1, 1, torch.float32).variant == "wide"     # <= 1024 (fp32)
     assert btd.Plan(4096, 32, 1, 1, torch.float32).variant == "persist"
     assert btd.Plan(8192, 32, 1, 65, torch.float64).variant == "wide"    # many right-hand sides
-    assert btd.Plan(1000, 32, 4, 1, torch.float64).variant == "persist"  # batched: 4 x 148 columns
+    assert btd.Plan(1000, 32, 4, 1, torch.float64).variant == "wide"     # batched fp64 n=32: <= 2048 columns
+    assert btd.Plan(1024, 16, 4, 1, torch.float64).variant == "persist"  # other batched: 4 x 148 columns
+    assert btd.Plan(1000, 32, 3, 1, torch.float32).variant == "persist"
     assert btd.Plan(256, 128, 1, 1, torch.float64).variant == "persist"
     assert btd.Plan(64, 16, 1, 1, torch.float64).variant == "wide"
     assert btd.Plan(8, 16, 1, 1, torch.float64).variant == "fused"
